@@ -1,0 +1,115 @@
+// k_index.cu - A2 indexer scan, materialising fp32 scores (unfused/debug path
+// and the per-row fallback of the fused path).  Bandwidth-bound: one 16-B
+// coalesced load per token per KV head (C = 8), shared by the G q-heads of
+// the group, so the sketch is read exactly once (SURVEY.md 7 hard part 1).
+#include "sd_common.cuh"
+#include "sd_internal.h"
+#include "sd_score.cuh"
+
+namespace sd {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanTok = 2048;   // tokens per CTA
+
+// grid = (ceil(max_seq_len / kScanTok), B*Hkv)
+template <int G>
+__global__ void __launch_bounds__(kScanThreads) sketch_score_kernel(
+    const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk,
+    const int* __restrict__ channel_ids, int C, const int* __restrict__ page_table,
+    const int* __restrict__ seq_lens, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
+  extern __shared__ float qc[];  // [G][C]
+  const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
+  const int Hq = Hkv * G;
+  const int N = __ldg(seq_lens + b);
+  for (int i = threadIdx.x; i < G * C; i += blockDim.x) {
+    const int j = i / C, c = i - j * C;
+    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
+    const size_t qe = ((size_t)b * Hq + g * G + j) * kD + ch;
+    qc[i] = q_dtype == SD_F32 ? reinterpret_cast<const float*>(q)[qe]
+                              : bf_lo(reinterpret_cast<const uint16_t*>(q)[qe]);
+  }
+  __syncthreads();
+  const int* pt = page_table + (size_t)b * max_pages;
+  const int tbeg = blockIdx.x * kScanTok;
+  const int tend = min(N, tbeg + kScanTok);
+  float* srow = scores + ((size_t)b * Hq + g * G) * ld;
+  for (int t = tbeg + threadIdx.x; t < tend; t += kScanThreads) {
+    const int page = __ldg(pt + (t >> 4));
+    const uint16_t* row = sk + sketch_row_elem(page, t & 15, g, Hkv, C);
+    float acc[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) acc[j] = 0.f;
+    for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(row + c0), qc + c0, C, acc);
+#pragma unroll
+    for (int j = 0; j < G; ++j) srow[(size_t)j * ld + t] = acc[j];
+  }
+}
+
+// Exact scores from the K pages: one half-warp per token row.
+template <class KV, int G>
+__global__ void __launch_bounds__(kScanThreads) exact_score_kernel(
+    const void* __restrict__ q, const void* __restrict__ kp, const int* __restrict__ page_table,
+    const int* __restrict__ seq_lens, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
+  const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
+  const int Hq = Hkv * G;
+  const int N = __ldg(seq_lens + b);
+  const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
+  float qf[G][8];
+#pragma unroll
+  for (int j = 0; j < G; ++j) load_q8<KV>(q, ((size_t)b * Hq + g * G + j) * kD + l16 * 8, qf[j]);
+  const int* pt = page_table + (size_t)b * max_pages;
+  const int tbeg = blockIdx.x * kScanTok;
+  const int tend = min(N, tbeg + kScanTok);
+  float* srow = scores + ((size_t)b * Hq + g * G) * ld;
+  // uniform trip count per warp: both half-warps iterate together
+  for (int t0 = tbeg; t0 < tend; t0 += kScanThreads / 16) {
+    int t = t0 + hw;
+    const bool ok = t < tend;
+    if (!ok) t = tbeg;
+    float kf[8];
+    KV::unpack(KV::load(kp, kv_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv) + l16 * 8), kf);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s = fmaf(qf[j][e], kf[e], s);
+      s = half_warp_sum(s);
+      if (ok && l16 == j) srow[(size_t)j * ld + t] = s;
+    }
+  }
+}
+
+template <int G>
+cudaError_t index_dispatch(const Geo& g, const sd_paged_kv& kv, const sd_sketch* sk, const void* q,
+                           float* scores, int ld, cudaStream_t st) {
+  dim3 grid((g.max_seq_len + kScanTok - 1) / kScanTok, g.B * g.Hkv);
+  if (sk) {
+    const size_t smem = sizeof(float) * G * sk->channels;
+    sketch_score_kernel<G><<<grid, kScanThreads, smem, st>>>(
+        q, g.kv_dtype, reinterpret_cast<const uint16_t*>(sk->pages), sk->channel_ids, sk->channels,
+        kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, scores, ld);
+  } else if (g.kv_dtype == SD_BF16) {
+    exact_score_kernel<KvBF16, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens,
+                                                                 g.max_pages, g.Hkv, scores, ld);
+  } else {
+    exact_score_kernel<KvF32, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens,
+                                                                g.max_pages, g.Hkv, scores, ld);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_index_score(const Geo& g, const sd_paged_kv& kv, const sd_sketch* sk,
+                               const void* q, float* scores, int ld, cudaStream_t st) {
+  switch (g.G) {
+    case 1: return index_dispatch<1>(g, kv, sk, q, scores, ld, st);
+    case 2: return index_dispatch<2>(g, kv, sk, q, scores, ld, st);
+    case 4: return index_dispatch<4>(g, kv, sk, q, scores, ld, st);
+    case 8: return index_dispatch<8>(g, kv, sk, q, scores, ld, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sd

@@ -1,0 +1,334 @@
+// sd_api.cu - the C ABI (include/sdattn.h): argument validation, budget
+// arithmetic, workspace carving and launch sequencing.  No compute happens on
+// the host and there is no CPU fallback: every entry point only enqueues
+// sm_100a kernels on the caller's stream.
+#include <math.h>
+#include <string.h>
+
+#include "sd_internal.h"
+
+namespace sd {
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, int k_max) {
+  WsLayout L;
+  size_t off = 256;  // error word + reserved
+  const size_t rows = (size_t)B * Hq;
+  L.part = off;
+  off = align256(off + rows * kMaxSplits * kPartStride * sizeof(float));
+  if (with_budget) {
+    L.ld = (max_seq_len + 63) & ~63;
+    L.k_max = k_max;
+    L.scores = off;
+    off = align256(off + rows * (size_t)L.ld * sizeof(float));
+    L.idx = off;
+    off = align256(off + rows * (size_t)k_max * sizeof(int));
+    L.counts = off;
+    off = align256(off + rows * sizeof(int));
+  }
+  L.total = off;
+  return L;
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+namespace {
+
+bool k_from_budget(const sd_budget* b, int N, int* k) {
+  if (b->k_fixed > 0) {
+    if (b->k_fixed > N) return false;
+    *k = b->k_fixed;
+    return true;
+  }
+  if (!(b->sparsity >= 1.0f)) return false;
+  double c = ceil((double)N / (double)b->sparsity);
+  *k = c < 1.0 ? 1 : (c > N ? N : (int)c);
+  return true;
+}
+
+sd_status check_geom(const sd_geometry* g, int max_seq_len, Geo* out) {
+  if (!g) return SD_ERR_INVALID_ARG;
+  if (g->batch < 1 || g->num_q_heads < 1 || g->num_kv_heads < 1 || g->head_dim < 1 ||
+      g->page_size < 1 || g->max_pages_per_seq < 1)
+    return SD_ERR_INVALID_ARG;
+  if (g->num_q_heads % g->num_kv_heads) return SD_ERR_INVALID_ARG;
+  for (int dt : {g->kv_dtype, g->q_dtype, g->out_dtype})
+    if (dt != SD_BF16 && dt != SD_F32) return SD_ERR_INVALID_ARG;
+  if (max_seq_len < 1 || (long long)max_seq_len > (long long)g->max_pages_per_seq * g->page_size)
+    return SD_ERR_INVALID_ARG;
+  const int G = g->num_q_heads / g->num_kv_heads;
+  if (g->head_dim != kHeadDim || g->page_size != kPageSize) return SD_ERR_UNSUPPORTED;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return SD_ERR_UNSUPPORTED;
+  if (g->kv_dtype != g->q_dtype) return SD_ERR_UNSUPPORTED;
+  out->B = g->batch;
+  out->Hq = g->num_q_heads;
+  out->Hkv = g->num_kv_heads;
+  out->G = G;
+  out->max_pages = g->max_pages_per_seq;
+  out->kv_dtype = g->kv_dtype;
+  out->out_dtype = g->out_dtype;
+  out->max_seq_len = max_seq_len;
+  return SD_OK;
+}
+
+sd_status check_kv(const sd_paged_kv* kv, bool need_v) {
+  if (!kv || !kv->k_pages || !kv->page_table || !kv->seq_lens || kv->num_pages < 1)
+    return SD_ERR_INVALID_ARG;
+  if (need_v && !kv->v_pages) return SD_ERR_INVALID_ARG;
+  return SD_OK;
+}
+
+sd_status check_sketch(const sd_sketch* sk) {
+  if (!sk) return SD_OK;
+  if (!sk->pages || !sk->channel_ids || sk->channels < 1) return SD_ERR_INVALID_ARG;
+  if (sk->channels > kHeadDim) return SD_ERR_INVALID_ARG;  // C <= D
+  if (sk->channels % 8) return SD_ERR_UNSUPPORTED;
+  return SD_OK;
+}
+
+sd_status check_budget(const sd_budget* b, int max_seq_len, int* k_max) {
+  if (!b) return SD_ERR_INVALID_ARG;
+  if (b->n_sink != 0 || b->n_local != 0 || b->heavy_fraction != 0.f) return SD_ERR_UNSUPPORTED;
+  if (b->k_fixed < 0) return SD_ERR_INVALID_ARG;
+  if (b->k_fixed == 0 && !(b->sparsity >= 1.0f)) return SD_ERR_INVALID_ARG;
+  if (!k_from_budget(b, max_seq_len, k_max)) return SD_ERR_INVALID_ARG;
+  return SD_OK;
+}
+
+sd_status check_ws(const void* ws, size_t ws_bytes, size_t need) {
+  if (!ws || ((uintptr_t)ws & 255) || ws_bytes < need) return SD_ERR_WORKSPACE;
+  return SD_OK;
+}
+
+sd_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SD_OK : SD_ERR_CUDA; }
+
+#define SD_TRY(x)                    \
+  do {                               \
+    sd_status _s = (x);              \
+    if (_s != SD_OK) return _s;      \
+  } while (0)
+#define SD_CUDA(x)                                  \
+  do {                                              \
+    if ((x) != cudaSuccess) return SD_ERR_CUDA;     \
+  } while (0)
+
+inline char* wsp(void* ws, size_t off) { return reinterpret_cast<char*>(ws) + off; }
+
+}  // namespace
+
+extern "C" {
+
+const char* sd_status_str(sd_status s) {
+  switch (s) {
+    case SD_OK: return "SD_OK";
+    case SD_ERR_INVALID_ARG: return "SD_ERR_INVALID_ARG";
+    case SD_ERR_UNSUPPORTED: return "SD_ERR_UNSUPPORTED";
+    case SD_ERR_WORKSPACE: return "SD_ERR_WORKSPACE";
+    case SD_ERR_CUDA: return "SD_ERR_CUDA";
+    case SD_ERR_DEVICE_CHECK: return "SD_ERR_DEVICE_CHECK";
+  }
+  return "SD_ERR_UNKNOWN";
+}
+
+const char* sd_version(void) { return "sdattn 0.1 (sm_100a)"; }
+
+sd_status sd_budget_k(const sd_budget* budget, int32_t N, int32_t* k) {
+  if (!budget || !k || N < 1) return SD_ERR_INVALID_ARG;
+  if (budget->k_fixed < 0) return SD_ERR_INVALID_ARG;
+  if (budget->k_fixed == 0 && !(budget->sparsity >= 1.0f)) return SD_ERR_INVALID_ARG;
+  int kk;
+  if (!k_from_budget(budget, N, &kk)) return SD_ERR_INVALID_ARG;
+  *k = kk;
+  return SD_OK;
+}
+
+sd_status sd_workspace_size(const sd_geometry* geom, const sd_budget* budget, int32_t max_seq_len,
+                            size_t* bytes) {
+  if (!bytes) return SD_ERR_INVALID_ARG;
+  Geo g;
+  SD_TRY(check_geom(geom, max_seq_len, &g));
+  int k_max = 0;
+  if (budget) SD_TRY(check_budget(budget, max_seq_len, &k_max));
+  *bytes = ws_layout(g.B, g.Hq, g.Hkv, max_seq_len, budget != nullptr, k_max).total;
+  return SD_OK;
+}
+
+sd_status sd_workspace_size_k(const sd_geometry* geom, int32_t max_seq_len, int32_t k_max, size_t* bytes) {
+  if (!bytes || k_max < 1) return SD_ERR_INVALID_ARG;
+  Geo g;
+  SD_TRY(check_geom(geom, max_seq_len, &g));
+  *bytes = ws_layout(g.B, g.Hq, g.Hkv, max_seq_len, true, k_max).total;
+  return SD_OK;
+}
+
+sd_status sd_clear_device_error(void* ws, sd_stream stream) {
+  if (!ws) return SD_ERR_WORKSPACE;
+  return cuda_status(cudaMemsetAsync(ws, 0, 256, (cudaStream_t)stream));
+}
+
+sd_status sd_read_device_error(const void* ws, int32_t* code, sd_stream stream) {
+  if (!ws || !code) return SD_ERR_INVALID_ARG;
+  int32_t v = 0;
+  SD_CUDA(cudaMemcpyAsync(&v, ws, sizeof(v), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  SD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  *code = v;
+  return v ? SD_ERR_DEVICE_CHECK : SD_OK;
+}
+
+sd_status sd_sparse_index_score(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
+                                const void* q, float* scores, int32_t ld, sd_stream stream) {
+  SD_TRY(check_kv(kv, false));
+  Geo g;
+  SD_TRY(check_geom(geom, kv->max_seq_len, &g));
+  SD_TRY(check_sketch(sketch));
+  if (!q || !scores || ld < kv->max_seq_len) return SD_ERR_INVALID_ARG;
+  return cuda_status(launch_index_score(g, *kv, sketch, q, scores, ld, (cudaStream_t)stream));
+}
+
+sd_status sd_topk_select(const sd_geometry* geom, const float* scores, int32_t ld, const int32_t* seq_lens,
+                         int32_t max_seq_len, const sd_budget* budget, int32_t* idx, int32_t* counts,
+                         int32_t k_max, void* ws, size_t ws_bytes, sd_stream stream) {
+  Geo g;
+  SD_TRY(check_geom(geom, max_seq_len, &g));
+  int kb;
+  SD_TRY(check_budget(budget, max_seq_len, &kb));
+  if (!scores || !seq_lens || !idx || !counts || ld < max_seq_len || k_max < kb) return SD_ERR_INVALID_ARG;
+  SD_TRY(check_ws(ws, ws_bytes, 256));
+  Budget bud{budget->sparsity, budget->k_fixed};
+  return cuda_status(launch_topk(g, scores, ld, seq_lens, bud, idx, counts, k_max,
+                                 reinterpret_cast<int*>(ws), (cudaStream_t)stream));
+}
+
+sd_status sd_sparse_gather_attend(const sd_geometry* geom, const sd_paged_kv* kv, const void* q,
+                                  const int32_t* idx, const int32_t* counts, int32_t k_max,
+                                  const float* weights, float scale, void* out, float* lse, void* ws,
+                                  size_t ws_bytes, sd_stream stream) {
+  SD_TRY(check_kv(kv, true));
+  Geo g;
+  SD_TRY(check_geom(geom, kv->max_seq_len, &g));
+  if (!q || !idx || !counts || !out || k_max < 1 || !(scale > 0.f) || !isfinite(scale))
+    return SD_ERR_INVALID_ARG;
+  const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, false, 0);
+  SD_TRY(check_ws(ws, ws_bytes, L.total));
+  const int rows = g.B * g.Hq;
+  const int splits = choose_splits(rows, k_max, 64);
+  float* part = reinterpret_cast<float*>(wsp(ws, L.part));
+  cudaStream_t st = (cudaStream_t)stream;
+  SD_CUDA(launch_attend_list(g, *kv, q, idx, counts, k_max, weights, scale, part, splits, 0,
+                             reinterpret_cast<int*>(ws), st));
+  return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
+}
+
+sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
+                                 const void* q, const sd_budget* budget, float scale, void* out, float* lse,
+                                 int32_t* idx_out, int32_t* counts_out, int32_t k_max_out, void* ws,
+                                 size_t ws_bytes, sd_stream stream) {
+  SD_TRY(check_kv(kv, true));
+  Geo g;
+  SD_TRY(check_geom(geom, kv->max_seq_len, &g));
+  SD_TRY(check_sketch(sketch));
+  int k_max;
+  SD_TRY(check_budget(budget, kv->max_seq_len, &k_max));
+  if (!q || !out || !(scale > 0.f) || !isfinite(scale)) return SD_ERR_INVALID_ARG;
+  if (idx_out && k_max_out < k_max) return SD_ERR_INVALID_ARG;
+  const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, true, k_max);
+  SD_TRY(check_ws(ws, ws_bytes, L.total));
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = reinterpret_cast<int*>(ws);
+  float* scores = reinterpret_cast<float*>(wsp(ws, L.scores));
+  int* idx = idx_out ? idx_out : reinterpret_cast<int*>(wsp(ws, L.idx));
+  const int ldi = idx_out ? k_max_out : k_max;
+  int* counts = counts_out ? counts_out : reinterpret_cast<int*>(wsp(ws, L.counts));
+  Budget bud{budget->sparsity, budget->k_fixed};
+  const int rows = g.B * g.Hq;
+  SD_CUDA(launch_index_score(g, *kv, sketch, q, scores, L.ld, st));
+  SD_CUDA(launch_topk(g, scores, L.ld, kv->seq_lens, bud, idx, counts, ldi, err, st));
+  const int splits = choose_splits(rows, k_max, 64);
+  float* part = reinterpret_cast<float*>(wsp(ws, L.part));
+  SD_CUDA(launch_attend_list(g, *kv, q, idx, counts, ldi, nullptr, scale, part, splits, 0, err, st));
+  return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
+}
+
+sd_status sd_dense_decode(const sd_geometry* geom, const sd_paged_kv* kv, const void* q, float scale,
+                          void* out, float* lse, void* ws, size_t ws_bytes, sd_stream stream) {
+  SD_TRY(check_kv(kv, true));
+  Geo g;
+  SD_TRY(check_geom(geom, kv->max_seq_len, &g));
+  if (!q || !out || !(scale > 0.f) || !isfinite(scale)) return SD_ERR_INVALID_ARG;
+  const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, false, 0);
+  SD_TRY(check_ws(ws, ws_bytes, L.total));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int splits = choose_splits(g.B * g.Hkv, kv->max_seq_len, 256);
+  float* part = reinterpret_cast<float*>(wsp(ws, L.part));
+  SD_CUDA(launch_dense(g, *kv, q, scale, part, splits, st));
+  return cuda_status(launch_merge_parts(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st));
+}
+
+sd_status sd_lse_merge(int32_t parts, int32_t rows, int32_t D, const float* part_o, const float* part_lse,
+                       sd_dtype out_dtype, void* out, float* lse, sd_stream stream) {
+  if (parts < 1 || rows < 1 || !part_o || !part_lse || !out) return SD_ERR_INVALID_ARG;
+  if (out_dtype != SD_BF16 && out_dtype != SD_F32) return SD_ERR_INVALID_ARG;
+  if (D != kHeadDim) return SD_ERR_UNSUPPORTED;
+  return cuda_status(launch_lse_merge(parts, rows, part_o, part_lse, out_dtype, out, lse, (cudaStream_t)stream));
+}
+
+sd_status sd_seqshard_local_topk(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
+                                 const void* q, const sd_budget* budget, const int32_t* global_seq_lens,
+                                 int32_t max_global_seq_len, float* cand_scores, int32_t* cand_idx,
+                                 int32_t k_max, void* ws, size_t ws_bytes, sd_stream stream) {
+  SD_TRY(check_kv(kv, false));
+  Geo g;
+  SD_TRY(check_geom(geom, kv->max_seq_len, &g));
+  SD_TRY(check_sketch(sketch));
+  int kg;
+  SD_TRY(check_budget(budget, max_global_seq_len, &kg));
+  if (!q || !global_seq_lens || !cand_scores || !cand_idx || k_max < kg ||
+      max_global_seq_len < kv->max_seq_len)
+    return SD_ERR_INVALID_ARG;
+  const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, true, k_max);
+  SD_TRY(check_ws(ws, ws_bytes, L.total));
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = reinterpret_cast<int*>(ws);
+  float* scores = reinterpret_cast<float*>(wsp(ws, L.scores));
+  int* counts = reinterpret_cast<int*>(wsp(ws, L.counts));
+  Budget bud{budget->sparsity, budget->k_fixed};
+  SD_CUDA(launch_index_score(g, *kv, sketch, q, scores, L.ld, st));
+  return cuda_status(launch_topk_shard(g, scores, L.ld, kv->seq_lens, global_seq_lens, bud, cand_idx,
+                                       counts, cand_scores, k_max, err, st));
+}
+
+sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv, const void* q,
+                                 const sd_budget* budget, const int32_t* global_seq_lens,
+                                 const float* all_cand, const int32_t* cand_idx, int32_t k_max,
+                                 int32_t parts, int32_t rank, float scale, float* part_o, float* part_lse,
+                                 void* ws, size_t ws_bytes, sd_stream stream) {
+  SD_TRY(check_kv(kv, true));
+  Geo g;
+  SD_TRY(check_geom(geom, kv->max_seq_len, &g));
+  if (!budget || (budget->n_sink | budget->n_local) || budget->heavy_fraction != 0.f) return SD_ERR_INVALID_ARG;
+  if (budget->k_fixed == 0 && !(budget->sparsity >= 1.0f)) return SD_ERR_INVALID_ARG;
+  if (!q || !global_seq_lens || !all_cand || !cand_idx || !part_o || !part_lse || k_max < 1 || parts < 1 ||
+      rank < 0 || rank >= parts || !(scale > 0.f))
+    return SD_ERR_INVALID_ARG;
+  const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, true, k_max);
+  SD_TRY(check_ws(ws, ws_bytes, L.total));
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = reinterpret_cast<int*>(ws);
+  int* surv = reinterpret_cast<int*>(wsp(ws, L.idx));
+  int* surv_cnt = reinterpret_cast<int*>(wsp(ws, L.counts));
+  Budget bud{budget->sparsity, budget->k_fixed};
+  SD_CUDA(launch_seqshard_cut(g, all_cand, cand_idx, parts, rank, global_seq_lens, bud, k_max, surv,
+                              surv_cnt, err, st));
+  const int rows = g.B * g.Hq;
+  const int splits = choose_splits(rows, k_max, 64);
+  float* part = reinterpret_cast<float*>(wsp(ws, L.part));
+  SD_CUDA(launch_attend_list(g, *kv, q, surv, surv_cnt, k_max, nullptr, scale, part, splits, 1, err, st));
+  // normalised (o, lse) per row for the cross-rank merge
+  SD_CUDA(launch_merge_parts(part, rows, splits, part_o, SD_F32, part_lse, st));
+  return SD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// sd_common.cuh - device primitives shared by the sdattn kernels (sm_100a).
+//
+// Layout contract (include/sdattn.h): head_dim D = 128, page_size = 16,
+// K/V pages [num_pages][16][Hkv][128] (NHD), sketch pages
+// [num_pages][Hkv][16][C] bf16.  One K or V row of one KV head is 256 B (bf16)
+// or 512 B (fp32) contiguous; a half-warp (16 lanes) covers it with one 16-B
+// (bf16) or two 16-B (fp32) vector loads per lane.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sdattn.h"
+
+namespace sd {
+
+constexpr int kD = 128;         // head_dim
+constexpr int kPS = 16;         // page size
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// ---------------------------------------------------------------- error word
+__device__ __forceinline__ void set_error(int* err, int code) {
+  if (err) atomicCAS(err, 0, code);
+}
+
+// ---------------------------------------------------------------- budget (A1)
+// k_b = max(1, ceil(N / S)) in double precision, or k_fixed.
+__device__ __forceinline__ int budget_k_dev(int N, float S, int k_fixed) {
+  if (k_fixed > 0) return k_fixed;
+  double q = (double)N / (double)S;
+  double c = ceil(q);
+  int k = c < 1.0 ? 1 : (c > (double)N ? N : (int)c);
+  return k;
+}
+
+// ---------------------------------------------------------------- radix keys
+// Order-preserving map fp32 -> uint32 (larger score -> larger key).  -0.0 is
+// canonicalised to +0.0 so that equal scores give equal keys (ties then go to
+// the lower index).  Scores are finite by precondition.
+__device__ __forceinline__ uint32_t score_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (u == 0x80000000u) u = 0u;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_score(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+// ---------------------------------------------------------------- loads
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_v4(const void* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+__device__ __forceinline__ void unpack_bf16x8(const uint4& v, float* f) {
+  f[0] = bf_lo(v.x); f[1] = bf_hi(v.x);
+  f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
+  f[4] = bf_lo(v.z); f[5] = bf_hi(v.z);
+  f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
+}
+
+// Element type traits: 8 consecutive elements of a row as raw vector(s).
+struct KvBF16 {
+  static constexpr int kBytes = 2;
+  struct Raw { uint4 a; };
+  __device__ __forceinline__ static Raw load(const void* base, size_t elem) {
+    Raw r; r.a = ldg_nc_v4(reinterpret_cast<const char*>(base) + elem * 2); return r;
+  }
+  __device__ __forceinline__ static void unpack(const Raw& r, float* f) { unpack_bf16x8(r.a, f); }
+};
+struct KvF32 {
+  static constexpr int kBytes = 4;
+  struct Raw { uint4 a, b; };
+  __device__ __forceinline__ static Raw load(const void* base, size_t elem) {
+    const char* p = reinterpret_cast<const char*>(base) + elem * 4;
+    Raw r; r.a = ldg_nc_v4(p); r.b = ldg_nc_v4(p + 16); return r;
+  }
+  __device__ __forceinline__ static void unpack(const Raw& r, float* f) {
+    f[0] = __uint_as_float(r.a.x); f[1] = __uint_as_float(r.a.y);
+    f[2] = __uint_as_float(r.a.z); f[3] = __uint_as_float(r.a.w);
+    f[4] = __uint_as_float(r.b.x); f[5] = __uint_as_float(r.b.y);
+    f[6] = __uint_as_float(r.b.z); f[7] = __uint_as_float(r.b.w);
+  }
+};
+
+// q row chunk (8 elements at d0) as fp32, q stored in the KV dtype.
+template <class KV>
+__device__ __forceinline__ void load_q8(const void* q, size_t elem, float* f) {
+  typename KV::Raw r;
+  if (KV::kBytes == 2) {
+    r.a = ldg_v4(reinterpret_cast<const char*>(q) + elem * 2);
+  } else {
+    const char* p = reinterpret_cast<const char*>(q) + elem * 4;
+    reinterpret_cast<uint4*>(&r)[0] = ldg_v4(p);
+    reinterpret_cast<uint4*>(&r)[1] = ldg_v4(p + 16);
+  }
+  KV::unpack(r, f);
+}
+
+// Element offset of row (page, slot, kv head g) in a [P][16][Hkv][128] pool.
+__device__ __forceinline__ size_t kv_row_elem(int page, int slot, int g, int Hkv) {
+  return ((size_t)(page * kPS + slot) * Hkv + g) * kD;
+}
+
+// Physical (page, slot) of logical token t of sequence b.
+__device__ __forceinline__ int token_page(const int* __restrict__ page_table, int max_pages, int b, int t) {
+  return __ldg(page_table + (size_t)b * max_pages + (t >> 4));
+}
+
+// ---------------------------------------------------------------- output store
+__device__ __forceinline__ void store_out(void* out, int out_dtype, size_t i, float v) {
+  if (out_dtype == SD_F32) {
+    reinterpret_cast<float*>(out)[i] = v;
+  } else {
+    uint32_t u = __float_as_uint(v);
+    // round to nearest even (finite inputs)
+    u += 0x7fffu + ((u >> 16) & 1u);
+    reinterpret_cast<uint16_t*>(out)[i] = (uint16_t)(u >> 16);
+  }
+}
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ float half_warp_sum(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
+}  // namespace sd

@@ -1,0 +1,85 @@
+// sd_internal.h - host-side launchers and workspace layout shared by the
+// C-ABI translation unit (sd_api.cu) and the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "sdattn.h"
+
+namespace sd {
+
+constexpr int kHeadDim = 128;       // the only compiled head_dim
+constexpr int kPageSize = 16;       // the only compiled page size
+constexpr int kMaxSplits = 64;      // split-k partial slots per (b, h) row
+constexpr int kPartStride = 128 + 2;  // {m (log2 domain), l, o[128] unnormalised}
+
+// Resolved, validated arguments passed from the C-ABI layer to launchers.
+struct Geo {
+  int B, Hq, Hkv, G, max_pages, kv_dtype, out_dtype;
+  int max_seq_len;
+};
+
+struct Budget {
+  float S;
+  int k_fixed;
+};
+
+// Workspace carve-up; every region is 256-byte aligned.  Computed identically
+// by sd_workspace_size and by every entry point.
+struct WsLayout {
+  size_t err = 0;            // int32 error word (+ reserved)
+  size_t part = 0;           // float [B*Hq][kMaxSplits][kPartStride]
+  size_t scores = 0;         // float [B*Hq][ld]        (budget != NULL)
+  int ld = 0;
+  size_t idx = 0;            // int32 [B*Hq][k_max]
+  size_t counts = 0;         // int32 [B*Hq]
+  int k_max = 0;
+  // fused path (sample-bracket select)
+  size_t thr = 0;            // uint32 [B*Hq][2] bracket keys (lo, hi)
+  size_t cnt = 0;            // int32 [B*Hq][4] counters (n_hi, n_mid, status, pad)
+  size_t cand = 0;           // uint64 [B*Hq][cand_cap] (key << 32 | ~token)
+  int cand_cap = 0;
+  size_t uni = 0;            // uint32 [B*Hkv][uni_cap] union rows (token | mask << 24)
+  size_t uni_cnt = 0;        // int32 [B*Hkv]
+  int uni_cap = 0;
+  size_t total = 0;
+};
+
+WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, int k_max);
+
+// ---- launchers (return cudaGetLastError()) ---------------------------------
+cudaError_t launch_index_score(const Geo& g, const sd_paged_kv& kv, const sd_sketch* sk,
+                               const void* q, float* scores, int ld, cudaStream_t st);
+
+cudaError_t launch_topk(const Geo& g, const float* scores, int ld, const int* seq_lens,
+                        Budget bud, int* idx, int* counts, int k_max, int* err,
+                        cudaStream_t st);
+
+cudaError_t launch_attend_list(const Geo& g, const sd_paged_kv& kv, const void* q,
+                               const int* idx, const int* counts, int k_max,
+                               const float* weights, float scale, float* part, int splits,
+                               int allow_empty, int* err, cudaStream_t st);
+
+cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const int* seq_lens,
+                              const int* global_lens, Budget bud, int* idx, int* counts,
+                              float* cand_scores, int k_max, int* err, cudaStream_t st);
+
+cudaError_t launch_seqshard_cut(const Geo& g, const float* all_cand, const int* cand_idx, int parts,
+                                int rank, const int* global_lens, Budget bud, int k_max, int* surv,
+                                int* surv_cnt, int* err, cudaStream_t st);
+
+cudaError_t launch_dense(const Geo& g, const sd_paged_kv& kv, const void* q, float scale,
+                         float* part, int splits, cudaStream_t st);
+
+// Combine `splits` unnormalised partials per row into out / lse.
+cudaError_t launch_merge_parts(const float* part, int rows, int splits, void* out,
+                               int out_dtype, float* lse, cudaStream_t st);
+
+// Combine normalised (o, lse) parts (cross-GPU partials).
+cudaError_t launch_lse_merge(int parts, int rows, const float* part_o, const float* part_lse,
+                             int out_dtype, void* out, float* lse, cudaStream_t st);
+
+int choose_splits(int rows, int work_per_row, int min_per_split);
+
+}  // namespace sd

@@ -1,0 +1,333 @@
+"""CUDA path vs the fp64 oracle, element by element, through the C ABI.
+
+Sizes span several CTA tiles (scan tile 2048 tokens, top-k tile 4096 keys,
+attention tile 16 rows) and ragged tails; edge cases cover N_b = 1, k = N,
+all-equal and duplicated keys, fp32 KV, ragged batches and weights.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from parity import (OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_selection, host_subcase, rel_err)
+
+pytestmark = pytest.mark.gpu
+
+SCALE = 1.0 / math.sqrt(128)
+
+
+def _dev(case):
+    return case.to("cuda")
+
+
+def _kv(sd, case):
+    return sd.KVCache.from_case(case), sd.SketchCache.from_case(case)
+
+
+# --------------------------------------------------------------------------- A2
+@pytest.mark.parametrize("dtype,mode", [(torch.bfloat16, "sketch"), (torch.bfloat16, "exact"),
+                                        (torch.float32, "exact"), (torch.float32, "sketch")])
+def test_index_score_matches_oracle(cuda_lib, dtype, mode):
+    sd = cuda_lib
+    lens = [1, 17, 2048, 4099, 5000]
+    case = workloads.make_case(len(lens), 16, 4, lens, dtype=dtype, seed=11)
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, sk = _kv(sd, dc)
+    sc = sd.sparse_index_score(dc.q, kv, sk if mode == "sketch" else None).cpu().double().numpy()
+    for b, N in enumerate(lens):
+        for h in range(16):
+            ref = oracle.index_scores(inp, b, h, mode)
+            M = np.abs(ref).max()
+            assert np.abs(sc[b, h, :N] - ref).max() <= 1e-6 * M + 1e-30, (b, h)
+
+
+# --------------------------------------------------------------------------- A3
+def _seeded_scores(B, H, lens, seed, kind):
+    g = torch.Generator().manual_seed(seed)
+    ld = (max(lens) + 63) // 64 * 64
+    s = torch.zeros((B, H, ld), dtype=torch.float32)
+    for b, N in enumerate(lens):
+        if kind == "normal":
+            s[b, :, :N] = torch.randn((H, N), generator=g)
+        elif kind == "ties":
+            s[b, :, :N] = torch.randint(-4, 5, (H, N), generator=g).float() * 0.25
+        elif kind == "equal":
+            s[b, :, :N] = 1.5
+        elif kind == "signed_zero":
+            v = torch.randint(0, 3, (H, N), generator=g).float() - 1.0
+            v[v == 0] = -0.0
+            v[:, ::3] = 0.0
+            s[b, :, :N] = v
+    return s
+
+
+@pytest.mark.parametrize("kind", ["normal", "ties", "equal", "signed_zero"])
+@pytest.mark.parametrize("S,k_fixed", [(50.0, 0), (10.0, 0), (1.0, 0), (2.5, 0), (1.0, 7)])
+def test_topk_select_bit_exact(cuda_lib, kind, S, k_fixed):
+    """Scores are a seeded INPUT to both sides, so the selection (an integer
+    decision) is taken on identical fp32 values and must match bit for bit."""
+    sd = cuda_lib
+    lens = [7, 17, 4096, 5003, 131]
+    B, H = len(lens), 4
+    s = _seeded_scores(B, H, lens, 5, kind)
+    seq = torch.tensor(lens, dtype=torch.int32)
+    idx, cnt = sd.topk_select(s.cuda(), seq.cuda(), max(lens), S=S, k_fixed=k_fixed)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b, N in enumerate(lens):
+        k = oracle.budget_k(S, N, k_fixed) if k_fixed <= N else None
+        for h in range(H):
+            if k is None:
+                continue
+            ref = oracle.topk_select(s[b, h, :N].double().numpy(), k)
+            assert cnt[b, h] == k
+            assert idx[b, h, :k].tolist() == ref.tolist(), (b, h)
+
+
+def test_topk_full_length_row(cuda_lib):
+    """One 131,072-key row (BASELINE cfg3 row length) with heavy ties."""
+    sd = cuda_lib
+    N = 131072
+    s = _seeded_scores(2, 2, [N, N - 5], 9, "ties")
+    idx, cnt = sd.topk_select(s.cuda(), torch.tensor([N, N - 5], dtype=torch.int32).cuda(), N, S=50.0)
+    for b, n in enumerate([N, N - 5]):
+        for h in range(2):
+            k = oracle.budget_k(50.0, n)
+            ref = oracle.topk_select(s[b, h, :n].double().numpy(), k)
+            assert idx[b, h, :k].cpu().tolist() == ref.tolist()
+
+
+# --------------------------------------------------------------------------- A4/A5
+@pytest.mark.parametrize("dtype,out_dtype", [(torch.bfloat16, torch.float32), (torch.bfloat16, torch.bfloat16),
+                                             (torch.float32, torch.float32)])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_gather_attend_matches_oracle(cuda_lib, dtype, out_dtype, weighted):
+    sd = cuda_lib
+    lens = [1, 40, 3000, 777]
+    B, Hq, Hkv = len(lens), 8, 2
+    case = workloads.make_case(B, Hq, Hkv, lens, dtype=dtype, seed=3)
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, _ = _kv(sd, dc)
+    rng = np.random.default_rng(0)
+    k_max = 1500
+    idx = np.full((B, Hq, k_max), -1, dtype=np.int32)
+    cnt = np.zeros((B, Hq), dtype=np.int32)
+    w = np.ones((B, Hq, k_max), dtype=np.float32)
+    for b, N in enumerate(lens):
+        for h in range(Hq):
+            c = int(rng.integers(1, min(N, k_max) + 1))
+            sel = np.sort(rng.choice(N, c, replace=False))
+            idx[b, h, :c] = sel
+            cnt[b, h] = c
+            if weighted:
+                w[b, h, :c] = rng.uniform(0.1, 5.0, c).astype(np.float32)
+    out, lse = sd.sparse_gather_attend(dc.q, kv, torch.from_numpy(idx).cuda(), torch.from_numpy(cnt).cuda(),
+                                       weights=torch.from_numpy(w).cuda() if weighted else None,
+                                       scale=SCALE, out_dtype=out_dtype)
+    sd.clear_device_error()
+    assert sd.read_device_error() == 0
+    out = out.float().cpu().numpy()
+    lse = lse.cpu().numpy()
+    tol = OUT_TOL_BF16 if out_dtype == torch.bfloat16 else (OUT_TOL_F32 if dtype == torch.float32 else 1e-4)
+    for b in range(B):
+        for h in range(Hq):
+            c = cnt[b, h]
+            ro, rl = oracle.attend_given(inp, b, h, idx[b, h, :c], SCALE,
+                                         w[b, h, :c].astype(np.float64) if weighted else None)
+            assert rel_err(out[b, h], ro) <= tol, (b, h, rel_err(out[b, h], ro))
+            check_lse(lse[b, h], rl)
+
+
+def test_gather_attend_device_errors(cuda_lib):
+    sd = cuda_lib
+    case = _dev(workloads.make_case(1, 4, 1, 100, seed=1))
+    kv, _ = _kv(sd, case)
+
+    def run(idx_rows, counts, weights=None):
+        sd.clear_device_error()
+        idx = torch.tensor(idx_rows, dtype=torch.int32).cuda()[None]
+        cnt = torch.tensor(counts, dtype=torch.int32).cuda()[None]
+        wt = None if weights is None else torch.tensor(weights, dtype=torch.float32).cuda()[None]
+        sd.sparse_gather_attend(case.q, kv, idx, cnt, weights=wt)
+        return sd.read_device_error()
+
+    ok = [[0, 5, 9], [1, 2, 3], [7, 8, 99], [0, 1, 2]]
+    assert run(ok, [3, 3, 3, 3]) == 0
+    assert run([[0, 5, 100], *ok[1:]], [3, 3, 3, 3]) == 1      # index >= N
+    assert run([[5, 5, 9], *ok[1:]], [3, 3, 3, 3]) == 2        # not strictly increasing
+    assert run(ok, [3, 0, 3, 3]) == 3                          # empty list
+    assert run(ok, [3, 3, 3, 3], [[1, 1, 0.0]] + [[1, 1, 1]] * 3) == 4   # weight <= 0
+    sd.clear_device_error()
+
+
+# --------------------------------------------------------------------------- A7
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_dense_matches_oracle(cuda_lib, G):
+    sd = cuda_lib
+    lens = [1, 33, 4097, 9000]
+    Hkv = 2
+    case = workloads.make_case(len(lens), Hkv * G, Hkv, lens, seed=G)
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, _ = _kv(sd, dc)
+    out, lse = sd.dense_decode(dc.q, kv, scale=SCALE, out_dtype=torch.float32)
+    ro, rl = oracle.dense_decode(inp, SCALE)
+    out, lse = out.cpu().numpy(), lse.cpu().numpy()
+    for b in range(len(lens)):
+        for h in range(Hkv * G):
+            assert rel_err(out[b, h], ro[b, h]) <= 1e-4
+            check_lse(lse[b, h], rl[b, h])
+
+
+def test_dense_fp32_cfg1(cuda_lib):
+    sd = cuda_lib
+    case = workloads.config_case("cfg1", seed=1)
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, _ = _kv(sd, dc)
+    out, lse = sd.dense_decode(dc.q, kv, scale=SCALE)
+    ro, rl = oracle.dense_decode(inp, SCALE)
+    for h in range(8):
+        assert rel_err(out[0, h].cpu().numpy(), ro[0, h]) <= OUT_TOL_F32
+
+
+# --------------------------------------------------------------------------- A6 fused
+def _check_fused(sd, case, S, mode, out_dtype=torch.float32, k_fixed=0, rows=None):
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, sk = _kv(sd, dc)
+    out, lse, idx, cnt = sd.sparse_decode_fused(dc.q, kv, sk if mode == "sketch" else None, S=S, k_fixed=k_fixed,
+                                                scale=SCALE, out_dtype=out_dtype, return_idx=True)
+    sd.clear_device_error()
+    out = out.float().cpu().numpy()
+    lse = lse.cpu().numpy()
+    idx = idx.cpu().numpy()
+    cnt = cnt.cpu().numpy()
+    tol = OUT_TOL_BF16 if out_dtype == torch.bfloat16 else (OUT_TOL_F32 if case.dtype == torch.float32 else 1e-4)
+    todo = rows if rows is not None else [(b, h) for b in range(case.B) for h in range(case.Hq)]
+    for b, h in todo:
+        N = int(case.seq_lens[b])
+        k = oracle.budget_k(S, N, k_fixed)
+        scores = oracle.index_scores(inp, b, h, mode)
+        sel = check_selection(idx[b, h], cnt[b, h], scores, k)
+        ro, rl = oracle.attend_given(inp, b, h, sel, SCALE)
+        assert rel_err(out[b, h], ro) <= tol, (b, h, rel_err(out[b, h], ro))
+        check_lse(lse[b, h], rl)
+    return out, lse, idx, cnt
+
+
+@pytest.mark.parametrize("dist", ["iid", "needle", "dup", "equal", "spec"])
+def test_fused_sketch_matches_oracle(cuda_lib, dist):
+    lens = [1, 100, 4099, 20000]
+    case = workloads.make_case(len(lens), 32, 8, lens, seed=17, dist=dist, n_needles=64)
+    _check_fused(cuda_lib, case, 50.0, "sketch")
+
+
+@pytest.mark.parametrize("S", [1.0, 2.0, 10.0, 100.0, 500.0])
+def test_fused_exact_mode_sparsity_sweep(cuda_lib, S):
+    lens = [3, 257, 6000]
+    case = workloads.make_case(len(lens), 8, 2, lens, seed=23, sketch=False)
+    _check_fused(cuda_lib, case, S, "exact")
+
+
+def test_fused_cfg1_fp32_exact(cuda_lib):
+    """BASELINE.json configs[0]: B=1, 1 KV head, 8 q-heads, N=4096, S=50 (k=82), fp32 KV."""
+    case = workloads.config_case("cfg1")
+    out, lse, idx, cnt = _check_fused(cuda_lib, case, 50.0, "exact")
+    assert (cnt == 82).all()
+
+
+def test_fused_bf16_output_and_kfixed(cuda_lib):
+    case = workloads.make_case(2, 16, 2, [5000, 64], seed=31)
+    _check_fused(cuda_lib, case, 1.0, "sketch", out_dtype=torch.bfloat16, k_fixed=64)
+
+
+def test_fused_equals_unfused_chain(cuda_lib):
+    """The fused entry and sd_sparse_index_score -> sd_topk_select select the same
+    sets bit for bit (same fp32 score code) and give the same outputs."""
+    sd = cuda_lib
+    case = _dev(workloads.make_case(3, 32, 8, [7000, 30000, 123], seed=41, dist="needle", n_needles=40))
+    kv, sk = _kv(sd, case)
+    out_f, lse_f, idx_f, cnt_f = sd.sparse_decode_fused(case.q, kv, sk, S=20.0, scale=SCALE,
+                                                        out_dtype=torch.float32, return_idx=True)
+    sc = sd.sparse_index_score(case.q, kv, sk)
+    idx_u, cnt_u = sd.topk_select(sc, case.seq_lens, kv.max_seq_len, S=20.0, num_kv_heads=8)
+    assert torch.equal(cnt_f, cnt_u)
+    for b in range(3):
+        for h in range(32):
+            c = int(cnt_u[b, h])
+            assert torch.equal(idx_f[b, h, :c], idx_u[b, h, :c])
+    out_u, lse_u = sd.sparse_gather_attend(case.q, kv, idx_u, cnt_u, scale=SCALE, out_dtype=torch.float32)
+    assert (out_u - out_f).abs().max().item() <= 1e-5 * out_u.abs().max().item()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg2_s10", "cfg2_s100", "cfg3"])
+def test_fused_baseline_sizes_sampled_rows(cuda_lib, name):
+    """BASELINE.json full sizes in the bench's launch configuration; the oracle
+    checks sampled (b, h) rows one by one."""
+    sd = cuda_lib
+    cfg = workloads.CONFIGS[name]
+    case = workloads.config_case(name, device="cuda")
+    kv, sk = _kv(sd, case)
+    out, lse, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk, S=cfg["S"], scale=SCALE,
+                                                out_dtype=torch.float32, return_idx=True)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    for b in rng.choice(case.B, 2, replace=False):
+        sub = host_subcase(case, int(b))
+        inp = oracle.from_case(sub)
+        N = int(case.seq_lens[b])
+        k = oracle.budget_k(cfg["S"], N)
+        for h in rng.choice(case.Hq, 3, replace=False):
+            scores = oracle.index_scores(inp, 0, int(h), "sketch")
+            sel = check_selection(idx[b, h].cpu().numpy(), int(cnt[b, h]), scores, k)
+            ro, rl = oracle.attend_given(inp, 0, int(h), sel, SCALE)
+            assert rel_err(out[b, h].cpu().numpy(), ro) <= 1e-4
+            check_lse(float(lse[b, h]), rl)
+
+
+# --------------------------------------------------------------------------- sequence sharding (1 GPU)
+def _shard_kv(sd, case, lo, hi):
+    """KV cache view of tokens [lo, hi) of every sequence (lo page-aligned)."""
+    assert lo % 16 == 0
+    pt = case.page_table[:, lo // 16:].contiguous()
+    lens = torch.clamp(case.seq_lens - lo, min=0).clamp(max=hi - lo).to(torch.int32)
+    return sd.KVCache(case.k_pages, case.v_pages, pt, lens, max(1, int(lens.max()))), lens
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_seqshard_protocol_equals_fused(cuda_lib, P):
+    """Local top-k per shard -> all candidates -> global cut + local attend ->
+    LSE merge equals the unsharded fused result (indices bit-exact)."""
+    sd = cuda_lib
+    N = 8192
+    case = _dev(workloads.make_case(2, 16, 4, [N, N], seed=50 + P, dist="dup"))
+    kv, sk = _kv(sd, case)
+    S = 20.0
+    out_f, lse_f, idx_f, cnt_f = sd.sparse_decode_fused(case.q, kv, sk, S=S, scale=SCALE, out_dtype=torch.float32,
+                                                        return_idx=True)
+    bounds = [((r * N) // P) // 16 * 16 for r in range(P)] + [N]
+    glens = case.seq_lens
+    k_max = sd.budget_k(S, N)
+    cands, cidx, kvs = [], [], []
+    for r in range(P):
+        kvr, _ = _shard_kv(sd, case, bounds[r], bounds[r + 1])
+        cs, ci = sd.seqshard_local_topk(case.q, kvr, sk and sd.SketchCache(sk.pages, sk.channel_ids), glens, N, S,
+                                        k_max=k_max)
+        cands.append(cs)
+        cidx.append(ci)
+        kvs.append(kvr)
+    all_cand = torch.stack(cands).contiguous()
+    parts_o, parts_l, surv = [], [], []
+    for r in range(P):
+        po, pl = sd.seqshard_cut_attend(case.q, kvs[r], glens, all_cand, cidx[r], r, S, scale=SCALE)
+        parts_o.append(po)
+        parts_l.append(pl)
+    out, lse = sd.lse_merge(torch.stack(parts_o).contiguous(), torch.stack(parts_l).contiguous())
+    assert (out - out_f).abs().max().item() <= 2e-5 * out_f.abs().max().item()
+    assert (lse - lse_f).abs().max().item() <= 1e-4
