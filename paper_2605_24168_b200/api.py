@@ -305,6 +305,7 @@ def _ws_bytes_budget(g, bud, max_seq_len, k_max):
     return n.value
 
 
-# Kernel launches enqueued by one sd_sparse_decode_fused call (bench.py's
-# gpu_launches claim; keep in sync with csrc/sd_api.cu).
-LAUNCHES_PER_FUSED = 4
+# Kernel launches enqueued by one sd_sparse_decode_fused call in sketch mode
+# (sample, scan, select, attend_rows, merge) - bench.py's gpu_launches claim;
+# keep in sync with csrc/sd_api.cu.
+LAUNCHES_PER_FUSED = 5

@@ -3,7 +3,10 @@
 // the host and there is no CPU fallback: every entry point only enqueues
 // sm_100a kernels on the caller's stream.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <algorithm>
 
 #include "sd_internal.h"
 
@@ -26,9 +29,31 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
     off = align256(off + rows * (size_t)k_max * sizeof(int));
     L.counts = off;
     off = align256(off + rows * sizeof(int));
+    // fused sample-bracket select
+    L.thr = off;
+    off = align256(off + rows * 2 * sizeof(uint32_t));
+    L.cnt = off;
+    off = align256(off + rows * 4 * sizeof(int));
+    L.cand_cap = (int)((std::min<long long>((long long)max_seq_len, 2LL * k_max + 4096) + 63) & ~63LL);
+    L.cand = off;
+    off = align256(off + rows * (size_t)L.cand_cap * sizeof(unsigned long long));
+    const int G = Hq / Hkv;
+    L.uni_cap = (int)std::min<long long>((long long)max_seq_len, (long long)G * k_max);
+    L.uni = off;
+    off = align256(off + (size_t)B * Hkv * L.uni_cap * sizeof(uint32_t));
+    L.uni_cnt = off;
+    off = align256(off + (size_t)B * Hkv * sizeof(int));
   }
   L.total = off;
   return L;
+}
+
+int choose_row_splits(int groups, int rows_per_group, int resident_per_sm) {
+  const int target = 148 * resident_per_sm * 5;  // ~5 waves of resident CTAs
+  int s = (target + groups - 1) / std::max(groups, 1);
+  const int cap = std::max(1, (rows_per_group + 63) / 64);
+  s = std::min(s, cap);
+  return std::max(1, std::min(s, kMaxSplits));
 }
 
 }  // namespace sd
@@ -238,17 +263,46 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
   SD_TRY(check_ws(ws, ws_bytes, L.total));
   cudaStream_t st = (cudaStream_t)stream;
   int* err = reinterpret_cast<int*>(ws);
-  float* scores = reinterpret_cast<float*>(wsp(ws, L.scores));
-  int* idx = idx_out ? idx_out : reinterpret_cast<int*>(wsp(ws, L.idx));
-  const int ldi = idx_out ? k_max_out : k_max;
-  int* counts = counts_out ? counts_out : reinterpret_cast<int*>(wsp(ws, L.counts));
   Budget bud{budget->sparsity, budget->k_fixed};
   const int rows = g.B * g.Hq;
-  SD_CUDA(launch_index_score(g, *kv, sketch, q, scores, L.ld, st));
-  SD_CUDA(launch_topk(g, scores, L.ld, kv->seq_lens, bud, idx, counts, ldi, err, st));
-  const int splits = choose_splits(rows, k_max, 64);
   float* part = reinterpret_cast<float*>(wsp(ws, L.part));
-  SD_CUDA(launch_attend_list(g, *kv, q, idx, counts, ldi, nullptr, scale, part, splits, 0, err, st));
+  if (!sketch) {
+    // exact-score (oracle top-k) mode: materialised scores + radix top-k
+    float* scores = reinterpret_cast<float*>(wsp(ws, L.scores));
+    int* idx = idx_out ? idx_out : reinterpret_cast<int*>(wsp(ws, L.idx));
+    const int ldi = idx_out ? k_max_out : k_max;
+    int* counts = counts_out ? counts_out : reinterpret_cast<int*>(wsp(ws, L.counts));
+    SD_CUDA(launch_index_score(g, *kv, nullptr, q, scores, L.ld, st));
+    SD_CUDA(launch_topk(g, scores, L.ld, kv->seq_lens, bud, idx, counts, ldi, err, st));
+    const int splits = choose_splits(rows, k_max, 64);
+    SD_CUDA(launch_attend_list(g, *kv, q, idx, counts, ldi, nullptr, scale, part, splits, 0, err, st));
+    return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
+  }
+  // sketch (Double Sparsity) mode: sample-bracket select, scores stay on chip
+  SbsBuffers w;
+  w.thr = reinterpret_cast<uint32_t*>(wsp(ws, L.thr));
+  w.cnt = reinterpret_cast<int*>(wsp(ws, L.cnt));
+  w.cand = reinterpret_cast<unsigned long long*>(wsp(ws, L.cand));
+  w.cand_cap = L.cand_cap;
+  w.scratch = reinterpret_cast<float*>(wsp(ws, L.scores));
+  w.ld = L.ld;
+  w.uni = reinterpret_cast<uint32_t*>(wsp(ws, L.uni));
+  w.uni_cnt = reinterpret_cast<int*>(wsp(ws, L.uni_cnt));
+  w.uni_cap = L.uni_cap;
+  w.idx_out = idx_out;
+  w.counts_out = counts_out;
+  w.k_max_out = idx_out ? k_max_out : 0;
+  const char* ff = getenv("SD_FORCE_FALLBACK");
+  w.force_fallback = (ff && ff[0] == '1') ? 1 : 0;
+  w.err = err;
+  SD_CUDA(launch_sbs_select(g, *kv, *sketch, q, bud, w, st));
+  if (g.kv_dtype == SD_BF16) {
+    const int splits = choose_row_splits(g.B * g.Hkv, L.uni_cap, 2);
+    SD_CUDA(launch_attend_rows_mma(g, *kv, q, w.uni, w.uni_cnt, w.uni_cap, scale, part, splits, st));
+    return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
+  }
+  const int splits = choose_row_splits(g.B * g.Hkv, L.uni_cap);
+  SD_CUDA(launch_attend_rows(g, *kv, q, w.uni, w.uni_cnt, w.uni_cap, scale, part, splits, st));
   return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
 }
 
@@ -261,9 +315,13 @@ sd_status sd_dense_decode(const sd_geometry* geom, const sd_paged_kv* kv, const 
   const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, false, 0);
   SD_TRY(check_ws(ws, ws_bytes, L.total));
   cudaStream_t st = (cudaStream_t)stream;
-  const int splits = choose_splits(g.B * g.Hkv, kv->max_seq_len, 256);
+  const bool mma = g.kv_dtype == SD_BF16;
+  const int splits = choose_row_splits(g.B * g.Hkv, kv->max_seq_len, mma ? 2 : 3);
   float* part = reinterpret_cast<float*>(wsp(ws, L.part));
-  SD_CUDA(launch_dense(g, *kv, q, scale, part, splits, st));
+  if (mma)
+    SD_CUDA(launch_dense_rows_mma(g, *kv, q, scale, part, splits, st));
+  else
+    SD_CUDA(launch_dense_rows(g, *kv, q, scale, part, splits, st));
   return cuda_status(launch_merge_parts(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st));
 }
 

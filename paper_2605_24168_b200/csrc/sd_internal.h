@@ -82,4 +82,38 @@ cudaError_t launch_lse_merge(int parts, int rows, const float* part_o, const flo
 
 int choose_splits(int rows, int work_per_row, int min_per_split);
 
+// ---- fused sample-bracket select (k_fused.cu) -------------------------------
+struct SbsBuffers {
+  uint32_t* thr;                 // [B*Hq][2] bracket keys (lo, hi)
+  int* cnt;                      // [B*Hq][4] (n_sure, n_cand, status, pad)
+  unsigned long long* cand;      // [B*Hq][cand_cap] (key << 32 | token)
+  int cand_cap;
+  float* scratch;                // [B*Hq][ld] fallback scores
+  int ld;
+  uint32_t* uni;                 // [B*Hkv][uni_cap] union rows (token | mask << 24)
+  int* uni_cnt;                  // [B*Hkv]
+  int uni_cap;
+  int* idx_out;                  // optional [B*Hq][k_max_out]
+  int* counts_out;               // optional [B*Hq]
+  int k_max_out;
+  int force_fallback;
+  int* err;
+};
+
+cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
+                              Budget bud, const SbsBuffers& w, cudaStream_t st);
+
+// ---- row-list gather-attend (k_rows.cu) ---------------------------------------
+cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
+                               const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
+                               cudaStream_t st);
+cudaError_t launch_dense_rows(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
+                              int splits, cudaStream_t st);
+int choose_row_splits(int groups, int rows_per_group, int resident_per_sm = 3);
+cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
+                                   const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
+                                   cudaStream_t st);
+cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
+                                  int splits, cudaStream_t st);
+
 }  // namespace sd

@@ -337,3 +337,34 @@ def test_seqshard_protocol_equals_fused(cuda_lib, P):
     out, lse = sd.lse_merge(torch.stack(parts_o).contiguous(), torch.stack(parts_l).contiguous())
     assert (out - out_f).abs().max().item() <= 2e-5 * out_f.abs().max().item()
     assert (lse - lse_f).abs().max().item() <= 1e-4
+
+
+@pytest.mark.parametrize("dist", ["iid", "needle", "dup"])
+def test_fused_forced_fallback_identical(cuda_lib, dist, monkeypatch):
+    """The exact per-(b, g) fallback of the fused select gives the same index
+    sets and the same outputs as the sample-bracket fast path."""
+    sd = cuda_lib
+    case = _dev(workloads.make_case(2, 32, 8, [20000, 3000], seed=61, dist=dist, n_needles=100))
+    kv, sk = _kv(sd, case)
+    a = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, out_dtype=torch.float32, return_idx=True)
+    monkeypatch.setenv("SD_FORCE_FALLBACK", "1")
+    b = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, out_dtype=torch.float32, return_idx=True)
+    monkeypatch.delenv("SD_FORCE_FALLBACK")
+    assert torch.equal(a[3], b[3])
+    for bb in range(2):
+        for h in range(32):
+            c = int(a[3][bb, h])
+            assert torch.equal(a[2][bb, h, :c], b[2][bb, h, :c])
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_fused_deterministic_and_large_window(cuda_lib):
+    """Two calls are bitwise identical; N > one bitmap window (G=8 -> 65,536)."""
+    sd = cuda_lib
+    case = _dev(workloads.make_case(1, 16, 2, [70001], seed=71))
+    kv, sk = _kv(sd, case)
+    a = sd.sparse_decode_fused(case.q, kv, sk, S=100.0, scale=SCALE, out_dtype=torch.float32, return_idx=True)
+    b = sd.sparse_decode_fused(case.q, kv, sk, S=100.0, scale=SCALE, out_dtype=torch.float32, return_idx=True)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    _check_fused(sd, workloads.make_case(1, 16, 2, [70001], seed=71), 100.0, "sketch", rows=[(0, h) for h in range(16)])
