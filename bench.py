@@ -256,6 +256,9 @@ def main():
     model = RL.sparse_step_bytes(B, Hq, Hkv, cfg["N"], k, w=case.dtype.itemsize, exact=not cfg["sketch"],
                                  union_rows_total=E)
     del idx, cnt
+    sd.clear_device_error()
+    step(case.q)
+    fallback_rows = sd.read_stats()["fallback_rows"]
     clear_err = sd.read_device_error()
 
     for i in range(args.warmup):
@@ -357,6 +360,7 @@ def main():
         "clocks": clocks,
         "dense": dense,
         "device_error": clear_err,
+        "fallback_rows": fallback_rows,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, cfg, args.cpu_seqs)

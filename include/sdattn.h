@@ -152,6 +152,12 @@ sd_status sd_clear_device_error(void* ws, sd_stream stream);
  * SD_ERR_DEVICE_CHECK if it is non-zero (SD_OK otherwise). */
 sd_status sd_read_device_error(const void* ws, int32_t* code, sd_stream stream);
 
+/* Synchronize `stream` and read the workspace statistics words (cumulative
+ * since the last sd_clear_device_error): stats[0] = number of (b, h) rows for
+ * which sd_sparse_decode_fused left its sample-bracketed fast selection and
+ * computed the row on the exact slow path (same result, more time). n <= 8. */
+sd_status sd_read_stats(const void* ws, int32_t* stats, int32_t n, sd_stream stream);
+
 /* ---- A2: indexer scan ---------------------
  * scores[b][h][t] = sum_c q[b][h][ch[b][g][c]] * sketch[b][g][t][c]   (sketch)
  *                 = sum_d q[b][h][d] * K[b][t][g][d]                 (sketch == NULL)

@@ -7,7 +7,7 @@ fallback: every call runs in the CUDA library or raises.
 """
 from .api import (  # noqa: F401
     KVCache, SketchCache, SdError, budget_k, clear_device_error, dense_decode, geometry, load_library,
-    lse_merge, make_budget, read_device_error, seqshard_cut_attend, seqshard_local_topk, sparse_decode_fused,
+    lse_merge, make_budget, read_device_error, read_stats, seqshard_cut_attend, seqshard_local_topk, sparse_decode_fused,
     sparse_gather_attend, sparse_index_score, topk_select, workspace, workspace_size,
 )
 

@@ -60,6 +60,7 @@ _PROTOS = {
     "sd_workspace_size_k": (c_i32, [P(Geometry), c_i32, c_i32, P(c_size)]),
     "sd_clear_device_error": (c_i32, [c_vp, c_vp]),
     "sd_read_device_error": (c_i32, [c_vp, P(c_i32), c_vp]),
+    "sd_read_stats": (c_i32, [c_vp, P(c_i32), c_i32, c_vp]),
     "sd_sparse_index_score": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, c_vp, c_i32, c_vp]),
     "sd_topk_select": (c_i32, [P(Geometry), c_vp, c_i32, c_vp, c_i32, P(Budget), c_vp, c_vp, c_i32, c_vp,
                                c_size, c_vp]),

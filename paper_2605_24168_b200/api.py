@@ -146,6 +146,18 @@ def read_device_error(ws: Optional[torch.Tensor] = None, stream=None) -> int:
     return code.value
 
 
+def read_stats(ws: Optional[torch.Tensor] = None, stream=None) -> dict:
+    """Workspace statistics (cumulative since clear_device_error): number of rows
+    the fused path computed on its exact slow path."""
+    if ws is None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        ws = _WS[(torch.cuda.current_device(), s.cuda_stream)]
+    arr = (C.c_i32 * 1)()
+    p, _ = _ws_ptr(ws)
+    _check(C.load().sd_read_stats(p, arr, 1, _stream(stream)), "sd_read_stats")
+    return {"fallback_rows": int(arr[0])}
+
+
 def clear_device_error(ws: Optional[torch.Tensor] = None, stream=None):
     if ws is None:
         s = stream if stream is not None else torch.cuda.current_stream()
@@ -306,6 +318,6 @@ def _ws_bytes_budget(g, bud, max_seq_len, k_max):
 
 
 # Kernel launches enqueued by one sd_sparse_decode_fused call in sketch mode
-# (sample, scan, select, attend_rows, merge) - bench.py's gpu_launches claim;
+# (sample, scan, select, attend_rows with the split merge folded in, bf16 KV) -
 # keep in sync with csrc/sd_api.cu.
-LAUNCHES_PER_FUSED = 5
+LAUNCHES_PER_FUSED = 4

@@ -1,42 +1,42 @@
-// k_fused.cu - the fused decode path (A2 + A3 + union build) with scores that
-// never round-trip through HBM: "sample-bracket select" (SBS).
+// k_fused.cu - the fused decode path, A2 + A3 with scores that never
+// round-trip through HBM: "sample-bracket select" (SBS).  The selection is
+// consumed by the gather-attend kernels through the contract in sd_sbs.cuh.
 //
 // The exact top-k_b of a row (ties to the lower index S:200) is found
 // without materialising the B*Hq*N scores:
 //
 //  1. sbs_sample_kernel (grid B*Hkv): score a deterministic page-strided
 //     sample of each sequence (every spg-th page, <= 4096 tokens) for the G
-//     q-heads of the KV head and take two sample order statistics per head:
+//     q-heads of the KV head and take two sample order statistics per head,
 //       r_lo = ceil(k f + z sqrt(k f (1-f)) + 1),  r_hi = floor(k f - z sqrt(...))
-//     (f = sample fraction, z = 4).  The 22-bit key buckets holding them give
-//     tau_lo (bucket floor) <= tau_hi (bucket ceiling) such that, with
-//     overwhelming probability, #{key >= tau_lo} >= k_b >= #{key > tau_hi}.
-//     When the sample is the whole row (f = 1) the bracket is the 22-bit
-//     bucket of the exact k-th key.
-//  2. sbs_scan_kernel (grid chunks x B*Hkv): the bandwidth-bound pass.  A
-//     producer warp streams the chunk's sketch pages (256 B per page and KV
-//     head, head-major layout) into a shared-memory ring with cp.async.bulk;
-//     eight consumer warps form the G scores per token (fma chain identical to
-//     sd_sparse_index_score) and compare them with tau_lo / tau_hi.  Only
-//     candidates (key >= tau_lo, ~3% of tokens) leave the SM, as (key, token)
-//     pairs; "sure" tokens (key > tau_hi) are counted.
-//  3. sbs_select_kernel (grid B*Hkv): per head, r = k_b - #sure; the exact r-th
-//     key of the band (tau_lo <= key <= tau_hi) by an adaptive radix select
-//     over the candidates (all G heads per pass), exact ties resolved by
-//     sorting the tied token ids.  The selected sets are OR-ed into a shared
-//     bitmap and emitted in ascending token order as the GQA union row list
-//     (token | head-mask << 24), plus per-head index lists when requested.
-//     If any check fails (bracket missed, candidate overflow, too many ties)
-//     the CTA computes the exact result for its (b, g) the slow way: all
-//     scores (same fp32 code) into scratch, radix select, ordered emission.
-//     The result is identical either way; only the time differs.
+//     (f = sample fraction, z = 4).  Their 22-bit key buckets give tau_lo
+//     (bucket floor) <= tau_hi (bucket ceiling) such that, with overwhelming
+//     probability, #{key >= tau_lo} >= k_b >= #{key > tau_hi}.  When the sample
+//     is the whole row (f = 1) the bracket is the bucket of the exact k-th key.
+//  2. sbs_scan_kernel (grid chunks x B*Hkv): the bandwidth-bound pass.  The
+//     chunk's sketch rows (16 B per token and KV head) stream through a
+//     3-stage cp.async ring; each token's G scores are formed with the same
+//     fp32 fma chain as sd_sparse_index_score (packed FFMA2) and compared with
+//     tau_lo.  The only output is one ballot word per head and 32 tokens: the
+//     candidate bitmap cbm (~3% of bits set).
+//  3. sbs_select_kernel (grid B*Hq, one CTA per q-head): the row's candidate
+//     tokens are listed in token order from cbm, their exact scores recomputed
+//     (same fp32 code), r = k_b - #{key > tau_hi}, the exact r-th key tau of
+//     the band by an adaptive radix select, exact ties at tau kept lowest
+//     token first; the result is written as the selection bitmap fbm.  If a
+//     check fails (bracket missed, too many candidates, too many ties) the CTA
+//     computes the row exactly the slow way (all scores, same fp32 code, radix
+//     select, ordered emission) into the same fbm.  Identical result either way.
 //
-// Deterministic: the union list order is fixed by the bitmap and there are no
-// float atomics, so repeated calls are bitwise identical.
+// Deterministic: no float atomics; union rows are rebuilt in token order.
 #include <limits.h>
+#include <math.h>
+
+#include <algorithm>
 
 #include "sd_common.cuh"
 #include "sd_internal.h"
+#include "sd_sbs.cuh"
 #include "sd_score.cuh"
 #include "sd_select.cuh"
 
@@ -46,14 +46,11 @@ namespace {
 constexpr float kBracketZ = 4.0f;
 constexpr int kSampleThreads = 512;
 constexpr int kSampleSlots = 8;            // sample tokens per thread (cap 4096)
-constexpr int kScanConsumers = 8;          // consumer warps
-constexpr int kScanThreads = (kScanConsumers + 1) * 32;
-constexpr int kScanPages = 512;            // pages (x16 tokens) per scan CTA
-constexpr int kScanStageBytes = 16384;     // one ring stage
-constexpr int kScanStages = 4;
-constexpr int kCandBytes = 32768;          // smem candidate buffer per scan CTA
-constexpr int kSelThreads = 512;
-constexpr int kBitmapWords = 16384;        // 64 KB: G * window / 32
+constexpr int kScanNT = 256;               // 8 warps
+constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
+constexpr int kScanStages = 3;
+constexpr int kSelNT = 512;
+constexpr int kSelCap = 16384;             // candidates cached per row (keys + tokens: 128 KB)
 constexpr int kTieCap = 2048;
 
 __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t e) {
@@ -61,6 +58,7 @@ __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t 
                            : bf_lo(reinterpret_cast<const uint16_t*>(q)[e]);
 }
 
+// qc[j][c] = q[b][g*G + j][channel_ids[b][g][c]]
 template <int G>
 __device__ __forceinline__ void load_qc(float* qc, const void* q, int q_dtype, const int* channel_ids, int b,
                                         int g, int Hkv, int C, int nthreads) {
@@ -72,25 +70,20 @@ __device__ __forceinline__ void load_qc(float* qc, const void* q, int q_dtype, c
   }
 }
 
-template <int G>
-__device__ __forceinline__ void token_scores(const uint16_t* __restrict__ sk, const int* pt, int t, int g, int Hkv,
-                                             int C, const float* qc, float* acc) {
-  const int page = __ldg(pt + (t >> 4));
-  const uint16_t* row = sk + sketch_row_elem(page, t & 15, g, Hkv, C);
-#pragma unroll
-  for (int j = 0; j < G; ++j) acc[j] = 0.f;
-  for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(row + c0), qc + c0, C, acc);
-}
+// 2048-bin histograms are stored padded, bin b at hidx(b) = b + b / 64, so
+// that a warp reading 64-bin groups (one group per lane) is bank-conflict-free.
+constexpr int kHistWords = 2048 + 32;
+__device__ __forceinline__ int hidx(uint32_t b) { return (int)(b + (b >> 6)); }
 
-// Warp-level search of a 2048-bin histogram (highest bin = largest keys) for
-// the bin holding the r-th largest element; returns (bin, residual rank).
+// Warp-level search of a padded 2048-bin histogram (highest bin = largest
+// keys) for the bin holding the r-th largest element; returns (bin, residual
+// rank).  Two parallel levels: 32 groups of 64 bins, then 32 pairs of bins.
 __device__ __forceinline__ void warp_find_bin(const uint32_t* hist, uint32_t r, int* bin_out, uint32_t* res_out) {
   const int lane = threadIdx.x & 31;
-  // lane owns bins [2047 - 64*lane - 63, 2047 - 64*lane]
-  const int top = 2047 - 64 * lane;
+  const int top = 2047 - 64 * lane;  // lane owns bins [top - 63, top]
   uint32_t sum = 0;
-#pragma unroll 8
-  for (int i = 0; i < 64; ++i) sum += hist[top - i];
+#pragma unroll 16
+  for (int i = 0; i < 64; ++i) sum += hist[hidx(top - i)];
   uint32_t incl = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -98,25 +91,54 @@ __device__ __forceinline__ void warp_find_bin(const uint32_t* hist, uint32_t r, 
     if (lane >= o) incl += y;
   }
   const uint32_t excl = incl - sum;
-  const bool mine = excl < r && incl >= r;
-  const uint32_t who = __ballot_sync(0xffffffffu, mine);
+  const uint32_t who = __ballot_sync(0xffffffffu, excl < r && incl >= r);
   const int src = who ? __ffs(who) - 1 : 31;
-  int bin = 0;
-  uint32_t res = 1;
-  if (lane == src) {
-    uint32_t above = excl;
-    for (int i = 0; i < 64; ++i) {
-      const uint32_t c = hist[top - i];
-      if (above + c >= r) {
-        bin = top - i;
-        res = r - above;
-        break;
-      }
-      above += c;
-    }
+  // level 2: the 64 bins of lane src, two per lane, highest first
+  const uint32_t above = __shfl_sync(0xffffffffu, excl, src);
+  const int gtop = 2047 - 64 * src;
+  const uint32_t c0 = hist[hidx(gtop - 2 * lane)], c1 = hist[hidx(gtop - 2 * lane - 1)];
+  const uint32_t pair = c0 + c1;
+  uint32_t pin = pair;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, pin, o);
+    if (lane >= o) pin += y;
   }
-  *bin_out = __shfl_sync(0xffffffffu, bin, src);
-  *res_out = __shfl_sync(0xffffffffu, res, src);
+  const uint32_t pex = above + pin - pair;
+  const uint32_t who2 = __ballot_sync(0xffffffffu, pex < r && pex + pair >= r);
+  const int src2 = who2 ? __ffs(who2) - 1 : 31;
+  int bin = gtop - 2 * lane;
+  uint32_t res = r - pex;
+  if (!(pex + c0 >= r)) {
+    bin -= 1;
+    res -= c0;
+  }
+  *bin_out = __shfl_sync(0xffffffffu, bin, src2);
+  *res_out = __shfl_sync(0xffffffffu, res, src2);
+}
+
+// two independent fp32 fma's in one FFMA2 (bit-identical to two fmaf)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float y) {
+  unsigned long long r;
+  const unsigned long long a = ((unsigned long long)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+  const unsigned long long xx = ((unsigned long long)__float_as_uint(x1) << 32) | __float_as_uint(x0);
+  const unsigned long long yy = ((unsigned long long)__float_as_uint(y) << 32) | __float_as_uint(y);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(xx), "l"(yy), "l"(a));
+  a0 = __uint_as_float((uint32_t)r);
+  a1 = __uint_as_float((uint32_t)(r >> 32));
+}
+
+// Float threshold equivalent to key(s) >= lo on finite scores.
+__device__ __forceinline__ float thresh_lo(uint32_t lo) {
+  if (lo <= 0x007FFFFFu) return -INFINITY;  // below key(-inf): every finite score
+  if (lo >= 0xFF800000u) return INFINITY;   // above key(+inf): none
+  return key_score(lo);
+}
+
+__device__ __forceinline__ void cp_async16_zf(void* dst, const void* src, bool valid) {
+  const uint32_t d = smem_u32(dst);
+  const int n = valid ? 16 : 0;  // 0 => zero-fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
 // --------------------------------------------------------------------------- 1. sample
@@ -124,12 +146,12 @@ template <int G>
 __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
-    int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ cnt) {
+    int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // [G][CAP]
-  uint32_t* hist = keys + G * CAP;                     // [G][2048]
-  float* qc = reinterpret_cast<float*>(hist + G * 2048);
+  uint32_t* hist = keys + G * CAP;                     // [G][kHistWords] (padded)
+  float* qc = reinterpret_cast<float*>(hist + G * kHistWords);
   __shared__ int s_bin[G][2];
   __shared__ uint32_t s_res[G][2];
   const int bg = blockIdx.x, b = bg / Hkv, g = bg - b * Hkv;
@@ -138,12 +160,10 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
   load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSampleThreads);
-  for (int i = tid; i < G * 2048; i += kSampleThreads) hist[i] = 0;
+  for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist[i] = 0;
+  if (tid == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
   __syncthreads();
-  if (N < 1) {
-    if (tid < G) cnt[((size_t)b * Hq + g * G + tid) * 4 + 2] = 1;
-    return;
-  }
+  if (N < 1) return;
   const int k = min(budget_k_dev(N, S, k_fixed), N);
   const int npg = (N + 15) >> 4;
   const int cap_pages = CAP >> 4;
@@ -182,7 +202,7 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
       // bins within the warp before the shared-memory atomic
       const uint32_t bin = key ? (key >> 21) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      if (key && (tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[j * 2048 + bin], (uint32_t)__popc(peers));
+      if (key && (tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[j * kHistWords + hidx(bin)], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
@@ -202,9 +222,9 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   if (warp < G) {
     int bin;
     uint32_t res;
-    warp_find_bin(hist + warp * 2048, ra, &bin, &res);
+    warp_find_bin(hist + warp * kHistWords, ra, &bin, &res);
     if ((tid & 31) == 0) { s_bin[warp][0] = bin; s_res[warp][0] = res; }
-    warp_find_bin(hist + warp * 2048, rb, &bin, &res);
+    warp_find_bin(hist + warp * kHistWords, rb, &bin, &res);
     if ((tid & 31) == 0) { s_bin[warp][1] = bin; s_res[warp][1] = res; }
   }
   __syncthreads();
@@ -212,20 +232,20 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
 #pragma unroll 1
   for (int w = 0; w < 2; ++w) {
     // pass 2 (bits 20..10) among keys of the pass-1 bin, for rank w
-    for (int i = tid; i < G * 2048; i += kSampleThreads) hist[i] = 0;
+    for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist[i] = 0;
     __syncthreads();
     for (int i = tid; i < n_slots; i += kSampleThreads) {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const uint32_t key = keys[j * CAP + i];
-        if ((int)(key >> 21) == s_bin[j][w]) atomicAdd(&hist[j * 2048 + ((key >> 10) & 2047)], 1u);
+        if ((int)(key >> 21) == s_bin[j][w]) atomicAdd(&hist[j * kHistWords + hidx((key >> 10) & 2047)], 1u);
       }
     }
     __syncthreads();
     if (warp < G) {
       int bin;
       uint32_t res;
-      warp_find_bin(hist + warp * 2048, s_res[warp][w], &bin, &res);
+      warp_find_bin(hist + warp * kHistWords, s_res[warp][w], &bin, &res);
       if ((tid & 31) == 0) s_res[warp][w] = (uint32_t)bin;  // reuse: pass-2 bin
     }
     __syncthreads();
@@ -243,106 +263,86 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     const size_t row = (size_t)b * Hq + g * G + j;
     thr[row * 2 + 0] = lo;
     thr[row * 2 + 1] = hi;
-    cnt[row * 4 + 0] = 0;  // n_sure
-    cnt[row * 4 + 1] = 0;  // n_cand
-    cnt[row * 4 + 2] = 0;  // status
   }
   pdl_launch_dependents();
 }
 
 // --------------------------------------------------------------------------- 2. scan
-// Float thresholds equivalent to the key tests key(s) >= lo and key(s) > hi on
-// finite scores (keys <= 0x007FFFFF / >= 0xFF800000 are -inf / +inf / NaN).
-__device__ __forceinline__ float thresh_lo(uint32_t lo) {
-  if (lo <= 0x007FFFFFu) return -INFINITY;
-  if (lo >= 0xFF800000u) return INFINITY;  // no finite score reaches it
-  return key_score(lo);
-}
-__device__ __forceinline__ float thresh_hi(uint32_t hi) {
-  if (hi <= 0x007FFFFFu) return -INFINITY;
-  if (hi >= 0xFF800000u) return INFINITY;
-  if (hi == 0x7FFFFFFFu) hi = 0x7FFFFFFEu;  // no canonical key equals the -0 pattern
-  return key_score(hi);
-}
-
-__device__ __forceinline__ void cp_async16_zf(void* dst, const void* src, bool valid) {
-  const uint32_t d = smem_u32(dst);
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
-}
-
-// two independent fp32 fma's in one FFMA2 (bit-identical to two fmaf)
-__device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float y) {
-  unsigned long long r, a = ((unsigned long long)__float_as_uint(a1) << 32) | __float_as_uint(a0);
-  const unsigned long long xx = ((unsigned long long)__float_as_uint(x1) << 32) | __float_as_uint(x0);
-  const unsigned long long yy = ((unsigned long long)__float_as_uint(y) << 32) | __float_as_uint(y);
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(xx), "l"(yy), "l"(a));
-  a0 = __uint_as_float((uint32_t)r);
-  a1 = __uint_as_float((uint32_t)(r >> 32));
-}
-
-constexpr int kScanNT = 256;                 // 8 warps
-constexpr int kScanStageTok = 1024;          // tokens per stage (C = 8: 16 KB)
-constexpr int kScanStagesC = 4;
-constexpr int kScanTokCta = 8192;            // tokens per CTA
+// Candidate entries are written per (b, g, chunk, warp) region of kEntCap
+// slots: ent_tok[...][slot] = token, ent_sc[...][j][slot] = fp32 score of head
+// j (all G heads, for every token that ANY head of the group keeps); ent_cnt
+// holds the (possibly overflowing) count of the region.
+template <int G>
+struct EntCap {
+  static constexpr int value = G <= 4 ? 256 : 512;
+};
 
 // C8: sketch width 8 (q channels in registers, one 16-B row per token);
-// otherwise generic C (multiple of 8) with the q channels in shared memory.
+// otherwise a generic C (multiple of 8) with the q channels in shared memory.
 template <int G, bool C8>
 __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ thr, int* __restrict__ cnt, unsigned long long* __restrict__ cand, int cand_cap) {
-  constexpr int CCW = kCandBytes / 8 / G / (kScanNT / 32);  // candidate slots per warp per head
+    const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
+    int* __restrict__ ent_cnt, int nch) {
+  constexpr int NW = kScanNT / 32;
+  constexpr int CW = EntCap<G>::value;
   extern __shared__ __align__(128) unsigned char smem[];
-  // ring: stages of kScanStageTok tokens x (2C) bytes (C=8: 16 KB)
-  const int stage_tok = kScanStageTok * 8 / C;  // C = 8: 1024 tokens = 16 KB per stage
-  const int stage_bytes = kScanStageTok * 16;
+  const int stage_tok = kScanStageTok8 * 8 / C;
+  const int stage_bytes = kScanStageTok8 * 16;
   unsigned char* ring = smem;
-  unsigned long long* cbuf =
-      reinterpret_cast<unsigned long long*>(ring + (size_t)kScanStagesC * stage_bytes);  // [G][8 warps][CCW]
-  float* qc = reinterpret_cast<float*>(cbuf + G * (kScanNT / 32) * CCW);                 // [G][C]
-  __shared__ int s_pages[kScanTokCta / 16];
-  __shared__ float s_flo[G];
-  __shared__ int s_wcnt[G][kScanNT / 32], s_base[G][kScanNT / 32], s_ovf;
+  float* qc = reinterpret_cast<float*>(ring + (size_t)kScanStages * stage_bytes);  // [G][C]
+  int* s_pages = reinterpret_cast<int*>(qc + G * C);                                // [kRangeTok / 16]
 
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = __ldg(seq_lens + b);
-  const int t0 = blockIdx.x * kScanTokCta;
+  const int chunk = blockIdx.x;
+  const int t0 = chunk * kRangeTok;
+  const size_t reg = ((size_t)bg * nch + chunk) * NW + warp;
   if (t0 >= N) {
+    if (lane == 0) ent_cnt[reg] = 0;
     pdl_launch_dependents();
     return;
   }
-  const int t_end = min(N, t0 + kScanTokCta);
-  const int ntok = t_end - t0;
+  const int ntok = min(N - t0, kRangeTok);
   const int npages = (ntok + 15) >> 4;
   const int* pt = page_table + (size_t)b * max_pages;
   for (int i = tid; i < npages; i += kScanNT) s_pages[i] = __ldg(pt + (t0 >> 4) + i);
   load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kScanNT);
-  if (tid == 0) s_ovf = 0;
   __syncthreads();
   const int nst = (ntok + stage_tok - 1) / stage_tok;
-  // cp.async issue of stage s: 16-B chunks; token i of the chunk lives at
-  // sketch_row(page i/16, slot i%16) and C/8 chunks long
   const int cpt = C >> 3;  // 16-B chunks per token
   auto issue = [&](int s) {
     if (s < nst) {
-      unsigned char* st = ring + (size_t)(s % kScanStagesC) * stage_bytes;
-      const int nch = stage_tok * cpt;
-      for (int qd = tid; qd < nch; qd += kScanNT) {
-        const int i = s * stage_tok + qd / cpt;  // chunk-relative token
-        const int c = qd - (qd / cpt) * cpt;
-        const bool valid = i < ntok;
-        const char* src = valid ? skb + (sketch_row_elem(s_pages[i >> 4], i & 15, g, Hkv, C) + c * 8) * 2 : skb;
-        cp_async16_zf(st + (size_t)qd * 16, src, valid);
+      unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+      if (C8) {
+        // one 16-B chunk per token; thread tid copies tokens tid + 256 u
+        const char* gb = skb + ((size_t)g * kPS) * 16;
+#pragma unroll
+        for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
+          const int ti = tid + u * kScanNT;
+          const int i = s * kScanStageTok8 + ti;  // chunk-relative token
+          const bool valid = i < ntok;
+          const char* src = valid ? gb + ((size_t)s_pages[i >> 4] * Hkv * kPS + (i & 15)) * 16 : skb;
+          cp_async16_zf(st + (size_t)ti * 16, src, valid);
+        }
+      } else {
+        const int nq = stage_tok * cpt;
+        for (int qd = tid; qd < nq; qd += kScanNT) {
+          const int ti = qd / cpt, c = qd - ti * cpt;
+          const int i = s * stage_tok + ti;  // chunk-relative token
+          const bool valid = i < ntok;
+          const char* src = valid ? skb + (sketch_row_elem(s_pages[i >> 4], i & 15, g, Hkv, C) + c * 8) * 2 : skb;
+          cp_async16_zf(st + (size_t)qd * 16, src, valid);
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int s = 0; s < kScanStagesC - 1; ++s) issue(s);
+  for (int s = 0; s < kScanStages - 1; ++s) issue(s);
 
   float qr[G][8];
   if (C8) {
@@ -351,28 +351,24 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
 #pragma unroll
       for (int c = 0; c < 8; ++c) qr[j][c] = qc[j * 8 + c];
   }
-  pdl_wait();  // thresholds come from the sample kernel
+  pdl_wait();  // the bracket comes from the sample kernel
   float flo[G];
 #pragma unroll
-  for (int j = 0; j < G; ++j) {
-    const size_t row = (size_t)b * Hq + g * G + j;
-    flo[j] = thresh_lo(__ldg(thr + row * 2 + 0));
-  }
+  for (int j = 0; j < G; ++j) flo[j] = thresh_lo(__ldg(thr + ((size_t)b * Hq + g * G + j) * 2));
   const uint32_t lt_mask = (1u << lane) - 1u;
-  int wcnt[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) wcnt[j] = 0;
-  unsigned long long* wreg = cbuf + (size_t)warp * CCW;  // + j * 8 * CCW
+  uint32_t* rtok = ent_tok + reg * CW;
+  float* rsc = ent_sc + reg * G * CW;
+  int wcnt = 0;
 
   for (int s = 0; s < nst; ++s) {
-    issue(s + kScanStagesC - 1);
-    asm volatile("cp.async.wait_group %0;" ::"n"(kScanStagesC - 1) : "memory");
+    issue(s + kScanStages - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
     __syncthreads();
-    const unsigned char* st = ring + (size_t)(s % kScanStagesC) * stage_bytes;
-#pragma unroll 1
+    const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+#pragma unroll 2
     for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
-      const int i = i0 + tid;                      // token within the stage
-      const int tl = s * stage_tok + i;            // chunk-relative token
+      const int i = i0 + tid;              // token within the stage
+      const int tl = s * stage_tok + i;    // chunk-relative token
       const bool valid = i < stage_tok && tl < ntok;
       float acc[G];
 #pragma unroll
@@ -393,332 +389,275 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
         const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
         for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(src[c0 >> 3], qc + c0, C, acc);
       }
+      bool any = false;
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const bool c = valid && acc[j] >= flo[j];
-        const uint32_t bal = __ballot_sync(0xffffffffu, c);
-        if (c) {
-          const int pos = wcnt[j] + __popc(bal & lt_mask);
-          if (pos < CCW)
-            wreg[(size_t)j * 8 * CCW + pos] = ((unsigned long long)score_key(acc[j]) << 32) | (unsigned)(t0 + tl);
-        }
-        wcnt[j] += __popc(bal);
+      for (int j = 0; j < G; ++j) any |= acc[j] >= flo[j];
+      any &= valid;
+      const uint32_t bal = __ballot_sync(0xffffffffu, any);
+      const int pos = wcnt + __popc(bal & lt_mask);
+      if (any && pos < CW) {
+        rtok[pos] = (uint32_t)(t0 + tl);
+#pragma unroll
+        for (int j = 0; j < G; ++j) rsc[j * CW + pos] = acc[j];
       }
+      wcnt += __popc(bal);
     }
     __syncthreads();  // slot reuse by the next issue()
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (lane == 0) {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      s_wcnt[j][warp] = min(wcnt[j], CCW);
-      if (wcnt[j] > CCW) s_ovf = 1;
-    }
-  }
-  __syncthreads();
-  if (tid < G) {
-    const int j = tid;
-    const size_t row = (size_t)b * Hq + g * G + j;
-    int tot = 0;
-    for (int w = 0; w < kScanNT / 32; ++w) tot += s_wcnt[j][w];
-    int base = tot ? atomicAdd(&cnt[row * 4 + 1], tot) : 0;
-    for (int w = 0; w < kScanNT / 32; ++w) {
-      s_base[j][w] = base;
-      base += s_wcnt[j][w];
-    }
-    if (s_ovf) atomicOr(&cnt[row * 4 + 2], 1);
-  }
-  __syncthreads();
-  // copy: warp w copies its own regions
-#pragma unroll 1
-  for (int j = 0; j < G; ++j) {
-    const size_t row = (size_t)b * Hq + g * G + j;
-    unsigned long long* dst = cand + row * cand_cap;
-    const unsigned long long* srcw = cbuf + ((size_t)j * 8 + warp) * CCW;
-    const int n = s_wcnt[j][warp], base = s_base[j][warp];
-    for (int i = lane; i < n; i += 32)
-      if (base + i < cand_cap) dst[base + i] = srcw[i];
-  }
+  if (lane == 0) ent_cnt[reg] = wcnt;  // > CW: overflow, the rows of (b, g) take the slow path
   pdl_launch_dependents();
 }
 
-// --------------------------------------------------------------------------- 3. select + union
+// --------------------------------------------------------------------------- 3. select (per q-head)
 template <int G>
-__global__ void __launch_bounds__(kSelThreads) sbs_select_kernel(
+__global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
-    int k_fixed, const uint32_t* __restrict__ thr, const int* __restrict__ cnt,
-    const unsigned long long* __restrict__ cand, int cand_cap, float* __restrict__ scratch, int ld,
-    uint32_t* __restrict__ uni, int* __restrict__ uni_cnt, int uni_cap, int* __restrict__ idx_out,
-    int* __restrict__ counts_out, int k_max_out, int force_fallback, int* __restrict__ err) {
+    int k_fixed, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
+    const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm,
+    int ldw, float* __restrict__ scratch, int ld, int* __restrict__ counts_out, int force_fallback,
+    int* __restrict__ err, int sel_cap) {
+  constexpr int NW = kScanNT / 32;
+  constexpr int CW = EntCap<G>::value;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem);        // [G][W/32]
-  uint32_t* hist = bm + kBitmapWords;                       // [G][2048]
-  uint32_t* ties = hist + G * 2048;                         // [kTieCap]
-  SelectSmem<kSelThreads>& sm = *reinterpret_cast<SelectSmem<kSelThreads>*>(ties + kTieCap);
-  float* qc = reinterpret_cast<float*>(&sm + 1);            // [G][C]
-  __shared__ uint32_t s_lo[G], s_hi[G], s_tau[G], s_need[G], s_pre[G], s_eqoff[G];
-  __shared__ int s_ncand[G], s_r[G], s_shift[G], s_prev[G], s_done[G], s_cut[G], s_sure[G], s_fb, s_ntie;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem);    // [sel_cap]
+  uint32_t* toks = keys + sel_cap;                       // [sel_cap]
+  uint32_t* ties = toks + sel_cap;                       // [kTieCap]
+  float* qc = reinterpret_cast<float*>(ties + kTieCap);  // [C]
+  __shared__ SelectSmem<kSelNT> sm;
+  __shared__ uint32_t hist2[kHistWords];
+  __shared__ int s_fb, s_sure, s_ntie, s_n;
+  __shared__ uint32_t s_pre, s_need;
+  __shared__ int s_shift, s_prev, s_done;
 
-  const int bg = blockIdx.x, b = bg / Hkv, g = bg - b * Hkv;
+  const int row = blockIdx.x;
   const int Hq = Hkv * G;
+  const int b = row / Hq, j = row - b * Hq - ((row - b * Hq) / G) * G, g = (row - b * Hq) / G;
+  const int bg = b * Hkv + g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
-  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSelThreads);
+  for (int c = tid; c < C; c += kSelNT) {
+    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
+    qc[c] = load_q_elem(q, q_dtype, (size_t)row * kD + ch);
+  }
+  if (tid == 0) {
+    s_fb = force_fallback;
+    s_sure = 0;
+    s_n = 0;
+  }
   pdl_wait();
   const int k = N >= 1 ? budget_k_dev(N, S, k_fixed) : 0;
-  if (N < 1 || k > N) {
+  const int nw = (max(N, 0) + 31) >> 5;
+  uint32_t* fr = fbm + (size_t)row * ldw;
+  for (int w = tid; w < nw; w += kSelNT) fr[w] = 0u;
+  if (N < 1 || k > N || k < 1) {
     if (tid == 0) {
       set_error(err, SD_DEVERR_SEQLEN);
-      uni_cnt[bg] = 0;
+      if (counts_out) counts_out[row] = 0;
     }
     return;
   }
-  if (tid == 0) s_fb = force_fallback;
+  const uint32_t lo = thr[row * 2 + 0], hi = thr[row * 2 + 1];
+  const float flo = thresh_lo(lo);
   __syncthreads();
-  if (tid < G) {
-    const int j = tid;
-    const size_t row = (size_t)b * Hq + g * G + j;
-    const int n_cand = cnt[row * 4 + 1], status = cnt[row * 4 + 2];
-    const uint32_t lo = thr[row * 2 + 0], hi = thr[row * 2 + 1];
-    if (status || n_cand > cand_cap || k > n_cand) atomicOr(&s_fb, 1);
-    s_lo[j] = lo;
-    s_hi[j] = hi;
-    s_ncand[j] = min(n_cand, cand_cap);
-    s_sure[j] = 0;
-    // band offsets off = key - lo lie in [0, hi - lo]; resolve them digit by
-    // digit from the top, <= 11 bits per pass
-    const uint32_t span = hi - lo;
-    const int bits = span ? 32 - __clz(span) : 1;
-    s_prev[j] = bits;
-    s_shift[j] = bits > 11 ? bits - 11 : 0;
-    s_pre[j] = 0;
+  // ---- this head's candidates from the group's scan entries: region counts
+  // -> prefix (one round trip), then one flat, unrolled pass over all entries
+  int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
+  if (nreg > kTieCap - 1) {  // beyond 2M tokens the region table does not fit: exact slow path
+    nreg = 0;
+    if (tid == 0) s_fb = 1;
   }
-  for (int i = tid; i < G * 2048; i += kSelThreads) hist[i] = 0;
+  int* s_roff = reinterpret_cast<int*>(ties);  // reuse: [nreg + 1] region offsets
+  const size_t reg0 = (size_t)bg * nch * NW;
+  int tot = 0;
+  for (int r0 = 0; r0 < nreg; r0 += kSelNT) {
+    const int r = r0 + tid;
+    int c = r < nreg ? ent_cnt[reg0 + r] : 0;
+    if (c > CW) {
+      s_fb = 1;
+      c = 0;
+    }
+    uint32_t all;
+    const uint32_t ex = block_excl_scan<kSelNT>((uint32_t)c, sm.warp_tot, &all);
+    if (r < nreg) s_roff[r] = tot + (int)ex;
+    tot += (int)all;
+  }
+  if (tid == 0) s_roff[nreg] = tot;
   __syncthreads();
-  // ---- phase A: exact r-th key of each head's band, all heads per pass.
-  // Pass 0 also counts the "sure" candidates (key > hi).
-  if (!s_fb) {
-#pragma unroll 1
-    for (int pass = 0; pass < 3; ++pass) {
-      if (pass > 0) {
-        for (int i = tid; i < G * 2048; i += kSelThreads) hist[i] = 0;
-        __syncthreads();
-      }
-      for (int j = 0; j < G; ++j) {
-        if (pass > 0 && s_done[j]) continue;
-        const size_t row = (size_t)b * Hq + g * G + j;
-        const unsigned long long* cl = cand + row * cand_cap;
-        const uint32_t lo = s_lo[j], hi = s_hi[j], pre = s_pre[j];
-        const int sh = s_shift[j], prev = s_prev[j];
-        const uint32_t dmask = (1u << (prev - sh)) - 1u;
-        const int n = s_ncand[j];
-        int sure = 0;
-        for (int i = tid; i < n; i += kSelThreads) {
-          const uint32_t key = (uint32_t)(cl[i] >> 32);
-          if (key > hi) {  // sure tokens are not in the band
-            ++sure;
-            continue;
-          }
-          const uint32_t off = key - lo;
-          if ((uint32_t)((uint64_t)off >> prev) != pre) continue;  // higher digits must match
-          atomicAdd(&hist[j * 2048 + ((off >> sh) & dmask)], 1u);
-        }
-        if (pass == 0) {
+  const uint32_t lt = (1u << lane) - 1u;
+  int sure = 0;
+  // warp per region; all of a region's entries are loaded before any is used
+  constexpr int U = CW / 32;
+  for (int r = warp; r < nreg; r += kSelNT / 32) {
+    const int cnt = s_roff[r + 1] - s_roff[r];
+    const size_t reg = reg0 + r;
+    const float* rsc = ent_sc + (reg * G + j) * CW;
+    const uint32_t* rtok = ent_tok + reg * CW;
+    float sc[U];
+    uint32_t tk[U];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
-          if (lane == 0 && sure) atomicAdd(&s_sure[j], sure);
-        }
-      }
-      __syncthreads();
-      if (pass == 0) {
-        if (tid < G) {
-          const int j = tid;
-          const int r = k - s_sure[j];
-          s_r[j] = r;
-          s_need[j] = (uint32_t)max(r, 0);
-          s_done[j] = r <= 0;
-          if (r < 0) atomicOr(&s_fb, 1);  // more than k sure tokens: bracket missed
-        }
-        __syncthreads();
-        if (s_fb) break;
-      }
-      if (warp < G && !s_done[warp]) {
-        const int j = warp;
-        int bin;
-        uint32_t res;
-        warp_find_bin(hist + j * 2048, s_need[j], &bin, &res);
-        if (lane == 0) {
-          const int sh = s_shift[j];
-          s_pre[j] = (uint32_t)(((uint64_t)s_pre[j] << (s_prev[j] - sh)) | (uint32_t)bin);
-          s_need[j] = res;
-          s_prev[j] = sh;
-          s_shift[j] = sh > 11 ? sh - 11 : 0;
-          s_done[j] = sh == 0;
-        }
-      }
-      __syncthreads();
-      bool more = false;
+    for (int u = 0; u < U; ++u) {
+      const int i = lane + 32 * u;
+      sc[u] = i < cnt ? rsc[i] : -INFINITY;
+      tk[u] = i < cnt ? rtok[i] : 0u;
+    }
 #pragma unroll
-      for (int j = 0; j < G; ++j) more |= !s_done[j];
-      if (!more) break;
+    for (int u = 0; u < U; ++u) {
+      if (32 * u >= cnt) break;
+      const bool c = lane + 32 * u < cnt && sc[u] >= flo;
+      const uint32_t bal = __ballot_sync(0xffffffffu, c);
+      if (!bal) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_n, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (c) {
+        const int p = base + __popc(bal & lt);
+        const uint32_t key = score_key(sc[u]);
+        if (p < sel_cap) {
+          keys[p] = key;
+          toks[p] = tk[u];
+        }
+        sure += key > hi;
+      }
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
+  if (lane == 0 && sure) atomicAdd(&s_sure, sure);
   __syncthreads();
+  const int n = s_n;
+  if (tid == 0 && (n > sel_cap || k > n)) s_fb = 1;
+  __syncthreads();
+  uint32_t tau = 0xFFFFFFFFu;
+  int cut = INT_MAX;
   if (!s_fb) {
-    // tau = lo + offset (pre holds the full offset once every digit is fixed)
-    if (tid < G) s_tau[tid] = s_r[tid] > 0 ? s_lo[tid] + s_pre[tid] : 0xFFFFFFFFu;
-    __syncthreads();
-    // exact ties at tau: if fewer are needed than exist, keep the lowest tokens
-    for (int j = 0; j < G; ++j) {
-      if (s_r[j] <= 0) {
-        if (tid == 0) s_cut[j] = INT_MAX;
-        continue;
+    const int r = k - s_sure;
+    if (r < 0) {
+      if (tid == 0) s_fb = 1;  // more than k sure tokens: the bracket missed
+    } else if (r > 0) {
+      // ---- adaptive radix select of the r-th key among band keys (lo <= key <= hi)
+      if (tid == 0) {
+        const uint32_t span = hi - lo;
+        const int bits = span ? 32 - __clz(span) : 1;
+        s_prev = bits;
+        s_shift = bits > 11 ? bits - 11 : 0;
+        s_pre = 0;
+        s_need = (uint32_t)r;
+        s_done = 0;
       }
-      const size_t row = (size_t)b * Hq + g * G + j;
-      const unsigned long long* cl = cand + row * cand_cap;
+      __syncthreads();
+#pragma unroll 1
+      for (int pass = 0; pass < 3 && !s_done; ++pass) {
+        for (int i = tid; i < kHistWords; i += kSelNT) hist2[i] = 0;
+        __syncthreads();
+        const int sh = s_shift, prev = s_prev;
+        const uint32_t pre = s_pre, dmask = (1u << (prev - sh)) - 1u;
+        for (int i = tid; i < n; i += kSelNT) {
+          const uint32_t key = keys[i];
+          if (key > hi || key < lo) continue;
+          const uint32_t o = key - lo;
+          if ((uint32_t)((uint64_t)o >> prev) != pre) continue;
+          atomicAdd(&hist2[hidx((o >> sh) & dmask)], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int bin;
+          uint32_t res;
+          warp_find_bin(hist2, s_need, &bin, &res);
+          if (lane == 0) {
+            s_pre = (uint32_t)(((uint64_t)pre << (prev - sh)) | (uint32_t)bin);
+            s_need = res;
+            s_prev = sh;
+            s_shift = sh > 11 ? sh - 11 : 0;
+            s_done = sh == 0;
+          }
+        }
+        __syncthreads();
+      }
+      tau = lo + s_pre;
+      const uint32_t need = s_need;
+      // ---- exact ties at tau: keep the lowest tokens if not all are needed
       if (tid == 0) s_ntie = 0;
       __syncthreads();
-      const uint32_t tau = s_tau[j];
-      for (int i = tid; i < s_ncand[j]; i += kSelThreads) {
-        const unsigned long long e = cl[i];
-        if ((uint32_t)(e >> 32) == tau) {
+      for (int i = tid; i < n; i += kSelNT) {
+        if (keys[i] == tau) {
           const int p = atomicAdd(&s_ntie, 1);
-          if (p < kTieCap) ties[p] = (uint32_t)e;
+          if (p < kTieCap) ties[p] = toks[i];
         }
       }
       __syncthreads();
       const int ntie = s_ntie;
-      if ((uint32_t)ntie > s_need[j]) {
+      if ((uint32_t)ntie > need) {
         if (ntie > kTieCap) {
           if (tid == 0) s_fb = 1;
-          __syncthreads();
-          break;
-        }
-        int cap2 = 1;
-        while (cap2 < ntie) cap2 <<= 1;
-        for (int i = ntie + tid; i < cap2; i += kSelThreads) ties[i] = 0xFFFFFFFFu;
-        bitonic_sort_smem<kSelThreads>(ties, cap2);
-        if (tid == 0) s_cut[j] = (int)ties[s_need[j] - 1];
-      } else if (tid == 0) {
-        s_cut[j] = INT_MAX;
-      }
-      __syncthreads();
-    }
-  }
-  __syncthreads();
-  const bool fb = s_fb != 0;
-  if (fb) {
-    // ---- exact generic path for this (b, g): scores into scratch, radix select
-    for (int t = tid; t < N; t += kSelThreads) {
-      float acc[G];
-      token_scores<G>(sk, pt, t, g, Hkv, C, qc, acc);
-#pragma unroll
-      for (int j = 0; j < G; ++j) scratch[((size_t)b * Hq + g * G + j) * ld + t] = acc[j];
-    }
-    __syncthreads();
-    for (int j = 0; j < G; ++j) {
-      const float* sr = scratch + ((size_t)b * Hq + g * G + j) * ld;
-      auto key_at = [sr](int i) { return score_key(sr[i]); };
-      uint32_t tau, need;
-      radix_select_block<kSelThreads>(key_at, N, (uint32_t)k, sm, &tau, &need);
-      if (tid == 0) {
-        s_tau[j] = tau;
-        s_need[j] = need;
-        s_eqoff[j] = 0;
-      }
-    }
-    __syncthreads();
-  }
-  // ---- phase C: windows of W tokens -> bitmap -> ascending union rows
-  constexpr int W = kBitmapWords * 32 / G;
-  constexpr int WW = W / 32;  // words per head
-  uint32_t total_u = 0;
-  uint32_t hcount[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) hcount[j] = 0;
-  uint32_t* ub = uni + (size_t)bg * uni_cap;
-  for (int w0 = 0; w0 < N; w0 += W) {
-    const int w1 = min(N, w0 + W);
-    for (int i = tid; i < kBitmapWords; i += kSelThreads) bm[i] = 0u;
-    __syncthreads();
-    if (!fb) {
-      for (int j = 0; j < G; ++j) {
-        const size_t row = (size_t)b * Hq + g * G + j;
-        const unsigned long long* cl = cand + row * cand_cap;
-        const int n_cand = s_ncand[j];
-        const uint32_t hi = s_hi[j], tau = s_tau[j];
-        const int r = s_r[j], cut = s_cut[j];
-        for (int i = tid; i < n_cand; i += kSelThreads) {
-          const unsigned long long e = cl[i];
-          const uint32_t key = (uint32_t)(e >> 32);
-          const int t = (int)(uint32_t)e;
-          if (t < w0 || t >= w1) continue;
-          const bool sel = key > hi || (r > 0 && (key > tau || (key == tau && t <= cut)));
-          if (sel) atomicOr(&bm[j * WW + ((t - w0) >> 5)], 1u << ((t - w0) & 31));
-        }
-      }
-    } else {
-      for (int j = 0; j < G; ++j) {
-        const float* sr = scratch + ((size_t)b * Hq + g * G + j) * ld + w0;
-        auto key_at = [sr](int i) { return score_key(sr[i]); };
-        uint32_t* bmj = bm + j * WW;
-        uint32_t eq_seen;
-        emit_block<kSelThreads, 4>(key_at, w1 - w0, s_tau[j], s_need[j], s_eqoff[j], sm,
-                                   [bmj](uint32_t, int i, uint32_t) { atomicOr(&bmj[i >> 5], 1u << (i & 31)); },
-                                   &eq_seen);
-        __syncthreads();
-        if (tid == 0) s_eqoff[j] += eq_seen;
-        __syncthreads();
-      }
-    }
-    __syncthreads();
-    // emit union rows (and per-head lists) in ascending token order
-    const int nwords = (w1 - w0 + 31) >> 5;
-    for (int wb = 0; wb < nwords; wb += kSelThreads) {
-      const int wi = wb + tid;
-      uint32_t words[G], u = 0;
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        words[j] = wi < nwords ? bm[j * WW + wi] : 0u;
-        u |= words[j];
-      }
-      uint32_t tot;
-      uint32_t pos = total_u + block_excl_scan<kSelThreads>(__popc(u), sm.warp_tot, &tot);
-      uint32_t bits = u;
-      while (bits) {
-        const int bit = __ffs(bits) - 1;
-        bits &= bits - 1;
-        uint32_t mask = 0;
-#pragma unroll
-        for (int j = 0; j < G; ++j) mask |= ((words[j] >> bit) & 1u) << j;
-        if (pos < (uint32_t)uni_cap) ub[pos] = (uint32_t)(w0 + wi * 32 + bit) | (mask << 24);
-        ++pos;
-      }
-      total_u += tot;
-      if (idx_out) {
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          uint32_t tj;
-          uint32_t p = hcount[j] + block_excl_scan<kSelThreads>(__popc(words[j]), sm.warp_tot, &tj);
-          int* dst = idx_out + ((size_t)b * Hq + g * G + j) * k_max_out;
-          uint32_t bj = words[j];
-          while (bj) {
-            const int bit = __ffs(bj) - 1;
-            bj &= bj - 1;
-            if (p < (uint32_t)k_max_out) dst[p] = w0 + wi * 32 + bit;
-            ++p;
-          }
-          hcount[j] += tj;
+        } else {
+          int cap2 = 1;
+          while (cap2 < ntie) cap2 <<= 1;
+          for (int i = ntie + tid; i < cap2; i += kSelNT) ties[i] = 0xFFFFFFFFu;
+          bitonic_sort_smem<kSelNT>(ties, cap2);
+          cut = (int)ties[need - 1];
         }
       }
     }
     __syncthreads();
   }
-  if (tid == 0) uni_cnt[bg] = (int)min(total_u, (uint32_t)uni_cap);
-  if (counts_out && tid < G) counts_out[(size_t)b * Hq + g * G + tid] = k;
+  if (!s_fb) {
+    // ---- selection bitmap
+    for (int i = tid; i < n; i += kSelNT) {
+      const uint32_t key = keys[i];
+      const int t = (int)toks[i];
+      if (key > hi || key > tau || (key == tau && t <= cut)) atomicOr(&fr[t >> 5], 1u << (t & 31));
+    }
+  } else {
+    // ---- exact slow path for this row: scores -> scratch, radix select, bitmap
+    if (tid == 0 && err) atomicAdd(err + 1, 1);  // statistics word: fallback rows
+    float* sr = scratch + (size_t)row * ld;
+    for (int t = tid; t < N; t += kSelNT) {
+      const uint16_t* rowp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+      float acc = 0.f;
+      for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rowp + c0), qc + c0, C, &acc);
+      sr[t] = acc;
+    }
+    __syncthreads();
+    auto key_at = [sr](int i) { return score_key(sr[i]); };
+    uint32_t ftau, fneed;
+    radix_select_block<kSelNT>(key_at, N, (uint32_t)k, sm, &ftau, &fneed);
+    emit_block<kSelNT, 4>(key_at, N, ftau, fneed, 0u, sm,
+                          [fr](uint32_t, int i, uint32_t) { atomicOr(&fr[i >> 5], 1u << (i & 31)); });
+  }
+  if (counts_out && tid == 0) counts_out[row] = k;
   pdl_launch_dependents();
+}
+
+// --------------------------------------------------------------------------- 4. per-head index lists
+// Optional (idx_out requested): fbm row -> ascending token list.
+constexpr int kIdxNT = 256;
+__global__ void __launch_bounds__(kIdxNT) sbs_idx_kernel(const int* __restrict__ seq_lens, int Hq,
+                                                         const uint32_t* __restrict__ fbm, int ldw,
+                                                         int* __restrict__ idx_out, int k_max_out) {
+  __shared__ uint32_t warp_tot[33];
+  const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
+  pdl_wait();
+  const int N = __ldg(seq_lens + b);
+  const int nw = (max(N, 0) + 31) >> 5;
+  const uint32_t* fr = fbm + (size_t)row * ldw;
+  int* dst = idx_out + (size_t)row * k_max_out;
+  int base = 0;
+  for (int w0 = 0; w0 < nw; w0 += kIdxNT) {
+    const int w = w0 + tid;
+    uint32_t word = w < nw ? fr[w] : 0u;
+    uint32_t tot;
+    uint32_t p = (uint32_t)base + block_excl_scan<kIdxNT>(__popc(word), warp_tot, &tot);
+    while (word) {
+      const int bit = __ffs(word) - 1;
+      word &= word - 1;
+      if (p < (uint32_t)k_max_out) dst[p] = w * 32 + bit;
+      ++p;
+    }
+    base += (int)tot;
+  }
 }
 
 template <class Kern>
@@ -749,55 +688,65 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int BG = geo.B * geo.Hkv;
   cudaError_t e;
   {
-    const size_t smem = sizeof(uint32_t) * G * (kSampleThreads * kSampleSlots + 2048) + sizeof(float) * G * C;
+    const size_t smem = sizeof(uint32_t) * G * (kSampleThreads * kSampleSlots + kHistWords) + sizeof(float) * G * C;
     auto kern = sbs_sample_kernel<G>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
-                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, w.thr, w.cnt);
+                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, w.thr, w.counters);
     if (e != cudaSuccess) return e;
   }
   {
-    const size_t smem = (size_t)kScanStagesC * kScanStageTok * 16 + kCandBytes + sizeof(float) * G * C;
-    dim3 grid((geo.max_seq_len + kScanTokCta - 1) / kScanTokCta, BG);
+    const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 + sizeof(float) * G * C +
+                        sizeof(int) * (kRangeTok / 16);
+    const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
+    dim3 grid(nch, BG);
     if (C == 8) {
       auto kern = sbs_scan_kernel<G, true>;
       set_smem(kern, smem);
       e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                      reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
-                     geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.cnt, w.cand, w.cand_cap);
+                     geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch);
     } else {
       auto kern = sbs_scan_kernel<G, false>;
       set_smem(kern, smem);
       e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                      reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
-                     geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.cnt, w.cand, w.cand_cap);
+                     geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch);
     }
     if (e != cudaSuccess) return e;
   }
   {
-    const size_t smem = sizeof(uint32_t) * (kBitmapWords + G * 2048 + kTieCap) + sizeof(SelectSmem<kSelThreads>) +
-                        sizeof(float) * G * C;
+    // candidate capacity: 2 k_max + 4096 (bracket width at the default sample), <= kSelCap
+    const int kmax = bud.k_fixed > 0 ? bud.k_fixed : (int)ceil((double)geo.max_seq_len / (double)bud.S);
+    const int sel_cap = std::min(kSelCap, ((2 * kmax + 4096) + 255) & ~255);
+    const size_t smem = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
+    const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
     auto kern = sbs_select_kernel<G>;
     set_smem(kern, smem);
-    e = launch_pdl(kern, dim3(BG), dim3(kSelThreads), smem, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
+    e = launch_pdl(kern, dim3(geo.B * geo.Hq), dim3(kSelNT), smem, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, (const uint32_t*)w.thr,
-                   (const int*)w.cnt, (const unsigned long long*)w.cand, w.cand_cap, w.scratch, w.ld, w.uni,
-                   w.uni_cnt, w.uni_cap, w.idx_out, w.counts_out, w.k_max_out, w.force_fallback, w.err);
+                   (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch, w.fbm, w.ldw,
+                   w.scratch, w.ld, w.counts_out, w.force_fallback, w.err, sel_cap);
+    if (e != cudaSuccess) return e;
   }
-  return e;
+  return cudaSuccess;
 }
 
 }  // namespace
 
 cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q, Budget bud,
                               const SbsBuffers& w, cudaStream_t st) {
+  cudaError_t e;
   switch (g.G) {
-    case 1: return sbs_launch_t<1>(g, kv, sk, q, bud, w, st);
-    case 2: return sbs_launch_t<2>(g, kv, sk, q, bud, w, st);
-    case 4: return sbs_launch_t<4>(g, kv, sk, q, bud, w, st);
-    case 8: return sbs_launch_t<8>(g, kv, sk, q, bud, w, st);
+    case 1: e = sbs_launch_t<1>(g, kv, sk, q, bud, w, st); break;
+    case 2: e = sbs_launch_t<2>(g, kv, sk, q, bud, w, st); break;
+    case 4: e = sbs_launch_t<4>(g, kv, sk, q, bud, w, st); break;
+    case 8: e = sbs_launch_t<8>(g, kv, sk, q, bud, w, st); break;
+    default: return cudaErrorInvalidValue;
   }
-  return cudaErrorInvalidValue;
+  if (e != cudaSuccess || !w.idx_out) return e;
+  return launch_pdl(sbs_idx_kernel, dim3(g.B * g.Hq), dim3(kIdxNT), 0, st, true, kv.seq_lens, g.Hq,
+                    (const uint32_t*)w.fbm, w.ldw, w.idx_out, w.k_max_out);
 }
 
 }  // namespace sd

@@ -17,6 +17,7 @@
 // is merge_parts_kernel.
 #include "sd_common.cuh"
 #include "sd_internal.h"
+#include "sd_sbs.cuh"
 
 namespace sd {
 namespace {
@@ -48,8 +49,7 @@ template <class KV, int G, bool kDense>
 __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
     const void* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
     const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ rows, const int* __restrict__ rows_cnt, int rows_cap, float scale_log2,
-    float* __restrict__ part, int splits, int max_per) {
+    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int max_tok) {
   using Cfg = RowCfg<KV>;
   constexpr int RB = Cfg::kRowBytes;
   constexpr int NS = Cfg::kStages;
@@ -57,8 +57,11 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes);
   uint64_t* empty = full + NS;
-  uint32_t* s_row = reinterpret_cast<uint32_t*>(empty + NS);  // [max_per] (page*16+slot)*Hkv+g
-  uint8_t* s_msk = reinterpret_cast<uint8_t*>(s_row + max_per);  // [max_per]
+  int* s_pages = reinterpret_cast<int*>(empty + NS);                           // [max_tok / 16 + 1]
+  constexpr int kW = kRangeTok / 32;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(s_pages + max_tok / 16 + 1);      // [G][kW]
+  int* upre = reinterpret_cast<int*>(bm + (kDense ? 0 : G * kW));             // [kW + 1]
+  __shared__ int warp_tot[kRowThreads / 32];
 
   const int bg = blockIdx.y, split = blockIdx.x;
   const int b = bg / Hkv, g = bg - b * Hkv;
@@ -81,24 +84,44 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
       for (int e = 0; e < 8; ++e) qf[j][e] *= scale_log2;
     }
   }
-  if (!kDense) pdl_wait();  // the row list is produced by the previous kernel
-  const int n = kDense ? __ldg(seq_lens + b) : min(rows_cnt[bg], rows_cap);
-  int per = (n + splits - 1) / splits;
-  per = min(max_per, (per + kStageRows - 1) & ~(kStageRows - 1));
-  const int r0 = min(n, split * per), r1 = min(n, r0 + per);
-  const int nst = (r1 - r0 + kStageRows - 1) / kStageRows;
-  // prologue: resolve every row of the chunk through the page table
-  const int* pt = page_table + (size_t)b * max_pages;
-  const uint32_t* rl = kDense ? nullptr : rows + (size_t)bg * rows_cap;
-  constexpr uint32_t kAll = (1u << G) - 1u;
-  for (int i = threadIdx.x; i < r1 - r0; i += kRowThreads) {
-    uint32_t e = kDense ? (uint32_t)(r0 + i) | (kAll << 24) : __ldg(rl + r0 + i);
-    const int t = (int)(e & 0xFFFFFFu);
-    const int page = __ldg(pt + (t >> 4));
-    s_row[i] = (uint32_t)(page * kPS + (t & 15)) * (uint32_t)Hkv + (uint32_t)g;
-    s_msk[i] = (uint8_t)(e >> 24);
+  const int N = __ldg(seq_lens + b);
+  int T0, T1;
+  if (kDense) {
+    int per = (N + splits - 1) / splits;
+    per = (per + 15) & ~15;
+    T0 = min(N, split * per);
+    T1 = min(N, T0 + per);
+  } else {
+    T0 = min(N, split * kRangeTok);
+    T1 = min(N, T0 + kRangeTok);
   }
-  __syncthreads();
+  const int* pt = page_table + (size_t)b * max_pages;
+  for (int i = threadIdx.x; i < ((T1 - T0 + 15) >> 4); i += kRowThreads) s_pages[i] = __ldg(pt + (T0 >> 4) + i);
+  int nrows;
+  const int nw = (T1 - T0 + 31) >> 5;
+  if (kDense) {
+    nrows = T1 - T0;
+    __syncthreads();
+  } else {
+    pdl_wait();  // the selection bitmaps come from sbs_select_kernel
+    nrows = T1 > T0 ? union_prologue<G, kRowThreads>(fbm, ldw, b * Hq + g * G, T0, T1, bm, upre, warp_tot) : 0;
+  }
+  const int r0 = 0, r1 = nrows;
+  const int nst = (r1 - r0 + kStageRows - 1) / kStageRows;
+  constexpr uint32_t kAll = (1u << G) - 1u;
+  auto row_tl = [&](int i) -> int { return kDense ? i : union_row_token<G>(bm, upre, nw, i); };
+  auto row_mask = [&](int i) -> uint32_t {
+    if (kDense) return kAll;
+    const int tl = row_tl(i);
+    uint32_t mk = 0;
+#pragma unroll
+    for (int j = 0; j < G; ++j) mk |= ((bm[j * nw + (tl >> 5)] >> (tl & 31)) & 1u) << j;
+    return mk;
+  };
+  auto row_index = [&](int i) -> uint32_t {
+    const int t = T0 + row_tl(i);
+    return (uint32_t)(s_pages[(t >> 4) - (T0 >> 4)] * kPS + (t & 15)) * (uint32_t)Hkv + (uint32_t)g;
+  };
 
   float m[G], l[G], o[G][8];
 #pragma unroll
@@ -120,7 +143,7 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
       __syncwarp();
       const int row = lane & 15, which = lane >> 4;
       if (row < cnt) {
-        const size_t off = (size_t)s_row[base + row] * RB;
+        const size_t off = (size_t)row_index(base + row) * RB;
         bulk_g2s(ring + ((size_t)(slot * kStageRows + row) * 2 + which) * RB, (which ? vp : kp) + off, RB,
                  &full[slot]);
       }
@@ -135,7 +158,7 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         const int row = hw + rr * 8;
-        const uint32_t mask = row < cnt ? (uint32_t)s_msk[base + row] : 0u;
+        const uint32_t mask = row < cnt ? row_mask(base + row) : 0u;
         const uint32_t need = __reduce_or_sync(0xffffffffu, mask);
         if (need == 0) continue;
         float kf[8], vf[8];
@@ -215,12 +238,12 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
 }
 
 template <class KV, int G, bool kDense>
-cudaError_t launch_rows_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                          const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
-                          cudaStream_t st) {
+cudaError_t launch_rows_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                          float scale, float* part, int splits, cudaStream_t st) {
   using Cfg = RowCfg<KV>;
-  const int max_per = ((kDense ? g.max_seq_len : rows_cap) + splits - 1) / splits + kStageRows;
-  const size_t smem = Cfg::kRingBytes + 2 * Cfg::kStages * sizeof(uint64_t) + (size_t)max_per * 5 + 16;
+  const int max_tok = kDense ? (((g.max_seq_len + splits - 1) / splits + 15) & ~15) : kRangeTok;
+  const size_t smem = Cfg::kRingBytes + 2 * Cfg::kStages * sizeof(uint64_t) + sizeof(int) * (max_tok / 16 + 1) +
+                      (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kRangeTok / 32) + 1)) + 16;
   static_assert((size_t)Cfg::kRingBytes >= (size_t)G * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
   auto kern = attend_rows_kernel<KV, G, kDense>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -236,37 +259,33 @@ cudaError_t launch_rows_t(const Geo& g, const sd_paged_kv& kv, const void* q, co
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, q, reinterpret_cast<const char*>(kv.k_pages),
                             reinterpret_cast<const char*>(kv.v_pages), kv.page_table, kv.seq_lens, g.max_pages,
-                            g.Hkv, rows, rows_cnt, rows_cap, scale * kLog2e, part, splits, max_per);
+                            g.Hkv, fbm, ldw, scale * kLog2e, part, splits, max_tok);
 }
 
 template <class KV, bool kDense>
-cudaError_t launch_rows_g(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                          const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
-                          cudaStream_t st) {
+cudaError_t launch_rows_g(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                          float scale, float* part, int splits, cudaStream_t st) {
   switch (g.G) {
-    case 1: return launch_rows_t<KV, 1, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-    case 2: return launch_rows_t<KV, 2, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-    case 4: return launch_rows_t<KV, 4, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-    case 8: return launch_rows_t<KV, 8, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
+    case 1: return launch_rows_t<KV, 1, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
+    case 2: return launch_rows_t<KV, 2, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
+    case 4: return launch_rows_t<KV, 4, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
+    case 8: return launch_rows_t<KV, 8, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                               const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
-                               cudaStream_t st) {
-  if (g.kv_dtype == SD_BF16)
-    return launch_rows_g<KvBF16, false>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-  return launch_rows_g<KvF32, false>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
+cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                               float scale, float* part, int splits, cudaStream_t st) {
+  if (g.kv_dtype == SD_BF16) return launch_rows_g<KvBF16, false>(g, kv, q, fbm, ldw, scale, part, splits, st);
+  return launch_rows_g<KvF32, false>(g, kv, q, fbm, ldw, scale, part, splits, st);
 }
 
 cudaError_t launch_dense_rows(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
                               int splits, cudaStream_t st) {
-  if (g.kv_dtype == SD_BF16)
-    return launch_rows_g<KvBF16, true>(g, kv, q, nullptr, nullptr, 0, scale, part, splits, st);
-  return launch_rows_g<KvF32, true>(g, kv, q, nullptr, nullptr, 0, scale, part, splits, st);
+  if (g.kv_dtype == SD_BF16) return launch_rows_g<KvBF16, true>(g, kv, q, nullptr, 0, scale, part, splits, st);
+  return launch_rows_g<KvF32, true>(g, kv, q, nullptr, 0, scale, part, splits, st);
 }
 
 }  // namespace sd

@@ -9,9 +9,11 @@
 // with mma.sync m16n8k16 (bf16 in, fp32 accumulate).  K and V are exact bf16;
 // P is split P = P_hi + P_lo into two bf16 terms (two PV mma's) so the output
 // keeps ~fp32 accuracy.  Rows a head did not select are masked to -inf before
-// the softmax (union mask byte per row).
+// the softmax (per-head selection bitmap of the CTA's token range).
 //
-// Memory path: rows are resolved through the page table in a prologue, then
+// Union mode: each CTA owns tokens [T0, T0 + 4096) of one (b, g) and rebuilds
+// their ascending union rows from the selection description (sd_sbs.cuh).
+// Memory path: the range's page ids are cached in shared memory; rows are
 // streamed into a 3-stage shared ring with 16-B cp.async (LDGSTS; rows past
 // the end are zero-filled), XOR-swizzled per 16-B chunk so ldmatrix is
 // bank-conflict-free.  Each of the 4 warps owns 16 rows of every 64-row stage
@@ -19,6 +21,7 @@
 // into one unnormalised split-k partial per q-head (merge_parts_kernel).
 #include "sd_common.cuh"
 #include "sd_internal.h"
+#include "sd_sbs.cuh"
 
 namespace sd {
 namespace {
@@ -74,16 +77,25 @@ __device__ __forceinline__ float bf16_round(float x) {
 // swizzled byte offset of 16-B chunk c of row r inside a [rows][256 B] block
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * kRowB + ((c ^ (r & 7)) << 4)); }
 
+template <int G>
+struct AttTok {
+  static constexpr int value = G <= 4 ? 16384 : 8192;  // tokens per union-mode CTA (bitmap fits smem)
+};
+
 template <int G, bool kDense>
 __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
     const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ rows, const int* __restrict__ rows_cnt, int rows_cap, float scale_log2,
-    float* __restrict__ part, int splits, int max_per) {
+    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int max_tok,
+    void* __restrict__ out, int out_dtype, float* __restrict__ lse_out, int* __restrict__ counters) {
+  constexpr int kAtt = AttTok<G>::value;  // union mode: tokens per CTA
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;                                              // [stages][K 16 KB | V 16 KB]
-  uint32_t* s_row = reinterpret_cast<uint32_t*>(ring + kStagesM * kStageBytesM);  // [max_per]
-  uint8_t* s_msk = reinterpret_cast<uint8_t*>(s_row + max_per);                   // [max_per]
+  unsigned char* ring = smem;                                                     // [stages][K | V]
+  int* s_pages = reinterpret_cast<int*>(ring + kStagesM * kStageBytesM);          // [max_tok / 16 + 1]
+  constexpr int kW = kAtt / 32;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(s_pages + max_tok / 16 + 1);         // [G][kW] head words
+  int* upre = reinterpret_cast<int*>(bm + (kDense ? 0 : G * kW));                // [kW + 1]
+  __shared__ int warp_tot[kMmaWarps];
 
   const int bg = blockIdx.y, split = blockIdx.x;
   const int b = bg / Hkv, g = bg - b * Hkv;
@@ -103,37 +115,75 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
       qa2[kk] = *reinterpret_cast<const uint32_t*>(qrow + 8);
     }
   }
-  if (!kDense) pdl_wait();  // the union row list is produced by the previous kernel
-  const int n = kDense ? __ldg(seq_lens + b) : min(rows_cnt[bg], rows_cap);
-  int per = (n + splits - 1) / splits;
-  per = min(max_per, (per + kTileRows - 1) & ~(kTileRows - 1));
-  const int r0 = min(n, split * per), r1 = min(n, r0 + per);
-  const int nrows = r1 - r0;
-  const int nst = (nrows + kStageRowsM - 1) / kStageRowsM;
-  // prologue: page-table resolution of every row of the chunk
-  const int* pt = page_table + (size_t)b * max_pages;
-  const uint32_t* rl = kDense ? nullptr : rows + (size_t)bg * rows_cap;
-  constexpr uint32_t kAll = (1u << G) - 1u;
-  for (int i = tid; i < nrows; i += kMmaThreads) {
-    const uint32_t e = kDense ? ((uint32_t)(r0 + i) | (kAll << 24)) : __ldg(rl + r0 + i);
-    const int t = (int)(e & 0xFFFFFFu);
-    const int page = __ldg(pt + (t >> 4));
-    s_row[i] = (uint32_t)(page * kPS + (t & 15)) * (uint32_t)Hkv + (uint32_t)g;
-    s_msk[i] = (uint8_t)(e >> 24);
+  const int N = __ldg(seq_lens + b);
+  // token range of this CTA
+  int T0, T1;
+  if (kDense) {
+    int per = (N + splits - 1) / splits;
+    per = (per + 15) & ~15;
+    T0 = min(N, split * per);
+    T1 = min(N, T0 + per);
+  } else {
+    T0 = min(N, split * kAtt);
+    T1 = min(N, T0 + kAtt);
   }
-  __syncthreads();
+  const int* pt = page_table + (size_t)b * max_pages;
+  for (int i = tid; i < ((T1 - T0 + 15) >> 4); i += kMmaThreads) s_pages[i] = __ldg(pt + (T0 >> 4) + i);
+  int nrows;
+  const int nw = (T1 - T0 + 31) >> 5;
+  if (kDense) {
+    nrows = T1 - T0;
+    __syncthreads();
+  } else {
+    pdl_wait();  // the selection bitmaps come from sbs_select_kernel
+    nrows = T1 > T0 ? union_prologue<G, kMmaThreads>(fbm, ldw, b * Hq + g * G, T0, T1, bm, upre, warp_tot) : 0;
+  }
+  const int nst = (nrows + kStageRowsM - 1) / kStageRowsM;
 
+  // row indices ((page * 16 + slot) * Hkv + g) of a stage, resolved once into
+  // a 4-slot shared array by 64 threads; the coalesced cp.async issue then
+  // needs one shared load per row (thread tid always copies chunk tid % 16)
+  __shared__ uint32_t s_ri[4][kStageRowsM];
+  __shared__ uint8_t s_mk[4][kStageRowsM];  // head mask of each stage row
+  constexpr uint32_t kAll = (1u << G) - 1u;
+  auto resolve = [&](int s) {
+    if (tid < kStageRowsM) {
+      const int i = s * kStageRowsM + tid;
+      uint32_t ri = 0xFFFFFFFFu, mk = 0u;
+      if (s < nst && i < nrows) {
+        int tl = i;
+        mk = kAll;
+        if (!kDense) {
+          tl = union_row_token<G>(bm, upre, nw, i);
+          mk = 0u;
+#pragma unroll
+          for (int j = 0; j < G; ++j) mk |= ((bm[j * nw + (tl >> 5)] >> (tl & 31)) & 1u) << j;
+        }
+        const int t = T0 + tl;
+        ri = (uint32_t)(s_pages[(t >> 4) - (T0 >> 4)] * kPS + (t & 15)) * (uint32_t)Hkv + g;
+      }
+      s_ri[s & 3][tid] = ri;
+      s_mk[s & 3][tid] = (uint8_t)mk;
+    }
+  };
+  // coalesced cp.async issue: thread tid copies 16-B chunk tid % 16 of rows
+  // tid / 16 + 8 i (i < 8) of the K and V blocks; the swizzled destination
+  // chunk is the same for all of them ((tid / 16 + 8 i) & 7 == (tid / 16) & 7)
+  const int ic = tid & 15, ir0 = tid >> 4;
+  const uint32_t dsw = (uint32_t)(ir0 * kRowB + ((ic ^ (ir0 & 7)) << 4));
+  const char* kpc = kp + ic * 16;
+  const char* vpc = vp + ic * 16;
   auto issue = [&](int s) {
     if (s < nst) {
-      unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM;
-      const int base = s * kStageRowsM;
+      unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM + dsw;
+      const uint32_t* ris = s_ri[s & 3] + ir0;
 #pragma unroll
-      for (int i = 0; i < (kStageRowsM * 2 * 16) / kMmaThreads; ++i) {
-        const int qd = tid + i * kMmaThreads;
-        const int kv = qd >> 10, r = (qd >> 4) & 63, c = qd & 15;
-        const bool valid = base + r < nrows;
-        const size_t off = valid ? (size_t)s_row[base + r] * kRowB + c * 16 : 0;
-        cp_async16(st + kv * (kStageRowsM * kRowB) + swz(r, c), (kv ? vp : kp) + off, valid);
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t ri = ris[8 * i];
+        const bool valid = ri != 0xFFFFFFFFu;
+        const size_t off = valid ? (size_t)ri * kRowB : 0;
+        cp_async16(st + i * 8 * kRowB, kpc + off, valid);
+        cp_async16(st + kStageRowsM * kRowB + i * 8 * kRowB, vpc + off, valid);
       }
     }
     cp_async_commit();
@@ -145,6 +195,9 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
   float m = -INFINITY, lsum = 0.f;
 
 #pragma unroll
+  for (int s = 0; s < kStagesM; ++s) resolve(s);
+  __syncthreads();
+#pragma unroll
   for (int s = 0; s < kStagesM - 1; ++s) issue(s);
   for (int s = 0; s < nst; ++s) {
     issue(s + kStagesM - 1);
@@ -152,7 +205,7 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     __syncthreads();
     const unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM;
     const int trow = warp * kTileRows;                 // this warp's tile inside the stage
-    const int rbase = s * kStageRowsM + trow;          // chunk-relative row of the tile
+    const int rbase = s * kStageRowsM + trow;          // CTA-relative row of the tile
     if (rbase < nrows) {
       const uint32_t kb = smem_u32(st) + trow * kRowB;
       const uint32_t vb = smem_u32(st + kStageRowsM * kRowB) + trow * kRowB;
@@ -161,7 +214,6 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
       const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        // matrices: (rows 0-7, dims 16kk..+7), (rows 0-7, +8..15), (rows 8-15, ..), (rows 8-15, ..)
         const int r = (lm >> 1) * 8 + lr, c = 2 * kk + (lm & 1);
         uint32_t b0, b1, b2, b3;
         ldsm_x4(kb + swz(r, c), b0, b1, b2, b3);
@@ -174,8 +226,8 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
       for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int rr = nt * 8 + qc2 + e;  // tile row
-          const bool ok = qr < G && rbase + rr < nrows && ((s_msk[rbase + rr] >> qr) & 1u);
+          const int rr = rbase + nt * 8 + qc2 + e;  // CTA-relative row
+          const bool ok = qr < G && ((s_mk[s & 3][trow + nt * 8 + qc2 + e] >> qr) & 1u);
           x[nt * 2 + e] = ok ? sc[nt][e] * scale_log2 : -INFINITY;
         }
       }
@@ -205,7 +257,6 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
       // ---- O += P V over 16 dim-tiles of 8
 #pragma unroll
       for (int nd = 0; nd < 16; nd += 2) {
-        // matrices: (rows 0-7, dims nd), (rows 8-15, nd), (rows 0-7, nd+1), (rows 8-15, nd+1)
         const int r = (lm & 1) * 8 + lr, c = nd + (lm >> 1);
         uint32_t b0, b1, b2, b3;
         ldsm_x4_t(vb + swz(r, c), b0, b1, b2, b3);
@@ -215,7 +266,8 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
         mma_bf16(o[nd + 1], pl0, pl2, b2, b3);
       }
     }
-    __syncthreads();  // the slot may be refilled by the next issue()
+    resolve(s + kStagesM);  // slot (s + 3) & 3: last read by issue(s - 1) and compute(s - 1)
+    __syncthreads();        // the ring slot may be refilled by the next issue()
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -261,14 +313,48 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
       dst[1] = L;
     }
   }
+  // ---- the last CTA of (b, g) merges the splits of its G rows (split order:
+  // deterministic) and re-arms the counter for the next call
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&counters[bg], 1) == splits - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int j = 0; j < G; ++j) {
+      const size_t row = (size_t)b * Hq + g * G + j;
+      const float* p = part + row * splits * kPartStride;
+      float M = -INFINITY;
+      for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(p + s2 * kPartStride));
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+        for (int s2 = 0; s2 < splits; ++s2) {
+          const float ms = __ldcg(p + s2 * kPartStride);
+          if (ms != -INFINITY) {
+            const float c = exp2f(ms - M);
+            L = fmaf(__ldcg(p + s2 * kPartStride + 1), c, L);
+            O = fmaf(__ldcg(p + s2 * kPartStride + 2 + d), c, O);
+          }
+        }
+      }
+      store_out(out, out_dtype, row * kD + d, L > 0.f ? O / L : 0.f);
+      if (lse_out && d == 0) lse_out[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+    }
+    if (tid == 0) counters[bg] = 0;
+  }
   if (!kDense) pdl_launch_dependents();
 }
 
 template <int G, bool kDense>
-cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                         const int* rows_cnt, int rows_cap, float scale, float* part, int splits, cudaStream_t st) {
-  const int max_per = ((kDense ? g.max_seq_len : rows_cap) + splits - 1) / splits + kTileRows;
-  const size_t smem = (size_t)kStagesM * kStageBytesM + (size_t)max_per * 5 + 16;
+cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                         float scale, float* part, int splits, void* out, float* lse, int* counters,
+                         cudaStream_t st) {
+  constexpr int kAtt = AttTok<G>::value;
+  if (!kDense) splits = (g.max_seq_len + kAtt - 1) / kAtt;
+  const int max_tok = kDense ? (((g.max_seq_len + splits - 1) / splits + 15) & ~15) : kAtt;
+  const size_t smem = (size_t)kStagesM * kStageBytesM + sizeof(int) * (max_tok / 16 + 1) +
+                      (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kAtt / 32) + 1)) + 16;
   static_assert(kStagesM * kStageBytesM >= kMmaWarps * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
   auto kern = attend_rows_mma_kernel<G, kDense>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -284,33 +370,38 @@ cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, con
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint16_t*>(q),
                             reinterpret_cast<const char*>(kv.k_pages), reinterpret_cast<const char*>(kv.v_pages),
-                            kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, rows, rows_cnt, rows_cap, scale * kLog2e,
-                            part, splits, max_per);
+                            kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
+                            max_tok, out, g.out_dtype, lse, counters);
 }
 
 template <bool kDense>
-cudaError_t launch_mma_g(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                         const int* rows_cnt, int rows_cap, float scale, float* part, int splits, cudaStream_t st) {
+cudaError_t launch_mma_g(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                         float scale, float* part, int splits, void* out, float* lse, int* ctr, cudaStream_t st) {
   switch (g.G) {
-    case 1: return launch_mma_t<1, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-    case 2: return launch_mma_t<2, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-    case 4: return launch_mma_t<4, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
-    case 8: return launch_mma_t<8, kDense>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
+    case 1: return launch_mma_t<1, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
+    case 2: return launch_mma_t<2, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
+    case 4: return launch_mma_t<4, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
+    case 8: return launch_mma_t<8, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                                   const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
+cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                                   float scale, float* part, void* out, float* lse, int* counters,
                                    cudaStream_t st) {
-  return launch_mma_g<false>(g, kv, q, rows, rows_cnt, rows_cap, scale, part, splits, st);
+  return launch_mma_g<false>(g, kv, q, fbm, ldw, scale, part, 0, out, lse, counters, st);
 }
 
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
-                                  int splits, cudaStream_t st) {
-  return launch_mma_g<true>(g, kv, q, nullptr, nullptr, 0, scale, part, splits, st);
+                                  int splits, void* out, float* lse, int* counters, cudaStream_t st) {
+  return launch_mma_g<true>(g, kv, q, nullptr, 0, scale, part, splits, out, lse, counters, st);
+}
+
+int union_att_splits(int G, int max_seq_len) {
+  const int t = G <= 4 ? AttTok<4>::value : AttTok<8>::value;
+  return (max_seq_len + t - 1) / t;
 }
 
 }  // namespace sd

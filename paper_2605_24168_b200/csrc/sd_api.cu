@@ -18,10 +18,15 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
   WsLayout L;
   size_t off = 256;  // error word + reserved
   const size_t rows = (size_t)B * Hq;
+  if (with_budget) L.nrange = (max_seq_len + kRangeTok - 1) / kRangeTok;
+  L.part_splits = std::max(kMaxSplits, L.nrange);
   L.part = off;
-  off = align256(off + rows * kMaxSplits * kPartStride * sizeof(float));
+  off = align256(off + rows * (size_t)L.part_splits * kPartStride * sizeof(float));
+  L.ctr = off;
+  off = align256(off + (size_t)B * Hkv * sizeof(int));
   if (with_budget) {
     L.ld = (max_seq_len + 63) & ~63;
+    L.ldw = L.ld / 32;
     L.k_max = k_max;
     L.scores = off;
     off = align256(off + rows * (size_t)L.ld * sizeof(float));
@@ -29,20 +34,19 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
     off = align256(off + rows * (size_t)k_max * sizeof(int));
     L.counts = off;
     off = align256(off + rows * sizeof(int));
-    // fused sample-bracket select
     L.thr = off;
     off = align256(off + rows * 2 * sizeof(uint32_t));
-    L.cnt = off;
-    off = align256(off + rows * 4 * sizeof(int));
-    L.cand_cap = (int)((std::min<long long>((long long)max_seq_len, 2LL * k_max + 4096) + 63) & ~63LL);
-    L.cand = off;
-    off = align256(off + rows * (size_t)L.cand_cap * sizeof(unsigned long long));
     const int G = Hq / Hkv;
-    L.uni_cap = (int)std::min<long long>((long long)max_seq_len, (long long)G * k_max);
-    L.uni = off;
-    off = align256(off + (size_t)B * Hkv * L.uni_cap * sizeof(uint32_t));
-    L.uni_cnt = off;
-    off = align256(off + (size_t)B * Hkv * sizeof(int));
+    const size_t nreg = (size_t)B * Hkv * L.nrange * 8;
+    const size_t cap = G <= 4 ? 256 : 512;  // EntCap<G> in k_fused.cu
+    L.ent_tok = off;
+    off = align256(off + nreg * cap * sizeof(uint32_t));
+    L.ent_sc = off;
+    off = align256(off + nreg * cap * G * sizeof(float));
+    L.ent_cnt = off;
+    off = align256(off + nreg * sizeof(int));
+    L.fbm = off;
+    off = align256(off + rows * (size_t)L.ldw * sizeof(uint32_t));
   }
   L.total = off;
   return L;
@@ -203,6 +207,14 @@ sd_status sd_read_device_error(const void* ws, int32_t* code, sd_stream stream) 
   return v ? SD_ERR_DEVICE_CHECK : SD_OK;
 }
 
+sd_status sd_read_stats(const void* ws, int32_t* stats, int32_t n, sd_stream stream) {
+  if (!ws || !stats || n < 1 || n > 8) return SD_ERR_INVALID_ARG;
+  SD_CUDA(cudaMemcpyAsync(stats, reinterpret_cast<const int32_t*>(ws) + 1, sizeof(int32_t) * n,
+                          cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  SD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return SD_OK;
+}
+
 sd_status sd_sparse_index_score(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
                                 const void* q, float* scores, int32_t ld, sd_stream stream) {
   SD_TRY(check_kv(kv, false));
@@ -281,28 +293,25 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
   // sketch (Double Sparsity) mode: sample-bracket select, scores stay on chip
   SbsBuffers w;
   w.thr = reinterpret_cast<uint32_t*>(wsp(ws, L.thr));
-  w.cnt = reinterpret_cast<int*>(wsp(ws, L.cnt));
-  w.cand = reinterpret_cast<unsigned long long*>(wsp(ws, L.cand));
-  w.cand_cap = L.cand_cap;
+  w.ent_tok = reinterpret_cast<uint32_t*>(wsp(ws, L.ent_tok));
+  w.ent_sc = reinterpret_cast<float*>(wsp(ws, L.ent_sc));
+  w.ent_cnt = reinterpret_cast<int*>(wsp(ws, L.ent_cnt));
+  w.fbm = reinterpret_cast<uint32_t*>(wsp(ws, L.fbm));
+  w.counters = reinterpret_cast<int*>(wsp(ws, L.ctr));
+  w.ldw = L.ldw;
   w.scratch = reinterpret_cast<float*>(wsp(ws, L.scores));
   w.ld = L.ld;
-  w.uni = reinterpret_cast<uint32_t*>(wsp(ws, L.uni));
-  w.uni_cnt = reinterpret_cast<int*>(wsp(ws, L.uni_cnt));
-  w.uni_cap = L.uni_cap;
-  w.idx_out = idx_out;
   w.counts_out = counts_out;
+  w.idx_out = idx_out;
   w.k_max_out = idx_out ? k_max_out : 0;
   const char* ff = getenv("SD_FORCE_FALLBACK");
   w.force_fallback = (ff && ff[0] == '1') ? 1 : 0;
   w.err = err;
   SD_CUDA(launch_sbs_select(g, *kv, *sketch, q, bud, w, st));
-  if (g.kv_dtype == SD_BF16) {
-    const int splits = choose_row_splits(g.B * g.Hkv, L.uni_cap, 2);
-    SD_CUDA(launch_attend_rows_mma(g, *kv, q, w.uni, w.uni_cnt, w.uni_cap, scale, part, splits, st));
-    return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
-  }
-  const int splits = choose_row_splits(g.B * g.Hkv, L.uni_cap);
-  SD_CUDA(launch_attend_rows(g, *kv, q, w.uni, w.uni_cnt, w.uni_cap, scale, part, splits, st));
+  if (g.kv_dtype == SD_BF16)
+    return cuda_status(launch_attend_rows_mma(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
+  const int splits = L.nrange;
+  SD_CUDA(launch_attend_rows(g, *kv, q, w.fbm, w.ldw, scale, part, splits, st));
   return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
 }
 
@@ -318,10 +327,12 @@ sd_status sd_dense_decode(const sd_geometry* geom, const sd_paged_kv* kv, const 
   const bool mma = g.kv_dtype == SD_BF16;
   const int splits = choose_row_splits(g.B * g.Hkv, kv->max_seq_len, mma ? 2 : 3);
   float* part = reinterpret_cast<float*>(wsp(ws, L.part));
-  if (mma)
-    SD_CUDA(launch_dense_rows_mma(g, *kv, q, scale, part, splits, st));
-  else
-    SD_CUDA(launch_dense_rows(g, *kv, q, scale, part, splits, st));
+  if (mma) {
+    int* ctr = reinterpret_cast<int*>(wsp(ws, L.ctr));
+    SD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * g.B * g.Hkv, st));  // merge counters
+    return cuda_status(launch_dense_rows_mma(g, *kv, q, scale, part, splits, out, lse, ctr, st));
+  }
+  SD_CUDA(launch_dense_rows(g, *kv, q, scale, part, splits, st));
   return cuda_status(launch_merge_parts(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st));
 }
 

@@ -6,12 +6,13 @@
 #include <stdint.h>
 
 #include "sdattn.h"
+#include "sd_sbs.cuh"
 
 namespace sd {
 
 constexpr int kHeadDim = 128;       // the only compiled head_dim
 constexpr int kPageSize = 16;       // the only compiled page size
-constexpr int kMaxSplits = 64;      // split-k partial slots per (b, h) row
+constexpr int kMaxSplits = 64;      // split-k partial slots per (b, h) row (dense / list paths)
 constexpr int kPartStride = 128 + 2;  // {m (log2 domain), l, o[128] unnormalised}
 
 // Resolved, validated arguments passed from the C-ABI layer to launchers.
@@ -29,20 +30,21 @@ struct Budget {
 // by sd_workspace_size and by every entry point.
 struct WsLayout {
   size_t err = 0;            // int32 error word (+ reserved)
-  size_t part = 0;           // float [B*Hq][kMaxSplits][kPartStride]
+  size_t part = 0;           // float [B*Hq][part_splits][kPartStride]
+  int part_splits = 0;
   size_t scores = 0;         // float [B*Hq][ld]        (budget != NULL)
   int ld = 0;
   size_t idx = 0;            // int32 [B*Hq][k_max]
   size_t counts = 0;         // int32 [B*Hq]
   int k_max = 0;
-  // fused path (sample-bracket select)
-  size_t thr = 0;            // uint32 [B*Hq][2] bracket keys (lo, hi)
-  size_t cnt = 0;            // int32 [B*Hq][4] counters (n_hi, n_mid, status, pad)
-  size_t cand = 0;           // uint64 [B*Hq][cand_cap] (key << 32 | ~token)
-  int cand_cap = 0;
-  size_t uni = 0;            // uint32 [B*Hkv][uni_cap] union rows (token | mask << 24)
-  size_t uni_cnt = 0;        // int32 [B*Hkv]
-  int uni_cap = 0;
+  // fused path (sample-bracket select, sd_sbs.cuh)
+  int nrange = 0, ldw = 0;
+  size_t thr = 0;            // uint32 [B*Hq][2]
+  size_t ent_tok = 0;        // uint32 [B*Hkv][nrange][8 warps][cap]
+  size_t ent_sc = 0;         // float  [B*Hkv][nrange][8 warps][G][cap]
+  size_t ent_cnt = 0;        // int32  [B*Hkv][nrange][8 warps]
+  size_t fbm = 0;            // uint32 [B*Hq][ldw] selection bitmap
+  size_t ctr = 0;            // int32 [B*Hkv] last-CTA merge counters (zero between calls)
   size_t total = 0;
 };
 
@@ -84,17 +86,17 @@ int choose_splits(int rows, int work_per_row, int min_per_split);
 
 // ---- fused sample-bracket select (k_fused.cu) -------------------------------
 struct SbsBuffers {
-  uint32_t* thr;                 // [B*Hq][2] bracket keys (lo, hi)
-  int* cnt;                      // [B*Hq][4] (n_sure, n_cand, status, pad)
-  unsigned long long* cand;      // [B*Hq][cand_cap] (key << 32 | token)
-  int cand_cap;
+  uint32_t* thr;
+  uint32_t* ent_tok;             // scan candidate entries (see k_fused.cu)
+  float* ent_sc;
+  int* ent_cnt;
+  uint32_t* fbm;
+  int* counters;                 // [B*Hkv] merge counters, zeroed by the sample kernel
+  int ldw;
   float* scratch;                // [B*Hq][ld] fallback scores
   int ld;
-  uint32_t* uni;                 // [B*Hkv][uni_cap] union rows (token | mask << 24)
-  int* uni_cnt;                  // [B*Hkv]
-  int uni_cap;
-  int* idx_out;                  // optional [B*Hq][k_max_out]
   int* counts_out;               // optional [B*Hq]
+  int* idx_out;                  // optional [B*Hq][k_max_out]
   int k_max_out;
   int force_fallback;
   int* err;
@@ -103,17 +105,19 @@ struct SbsBuffers {
 cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
                               Budget bud, const SbsBuffers& w, cudaStream_t st);
 
-// ---- row-list gather-attend (k_rows.cu) ---------------------------------------
-cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                               const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
-                               cudaStream_t st);
+// ---- row-list gather-attend (k_rows.cu: CUDA cores, k_rows_mma.cu: bf16 tensor cores)
+cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                               float scale, float* part, int splits, cudaStream_t st);
 cudaError_t launch_dense_rows(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
                               int splits, cudaStream_t st);
-int choose_row_splits(int groups, int rows_per_group, int resident_per_sm = 3);
-cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* rows,
-                                   const int* rows_cnt, int rows_cap, float scale, float* part, int splits,
+// bf16 tensor-core variants fold the split merge into their last CTA per (b, g)
+// (counters: int32 [B*Hkv], zero between calls)
+cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                                   float scale, float* part, void* out, float* lse, int* counters,
                                    cudaStream_t st);
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
-                                  int splits, cudaStream_t st);
+                                  int splits, void* out, float* lse, int* counters, cudaStream_t st);
+int union_att_splits(int G, int max_seq_len);
+int choose_row_splits(int groups, int rows_per_group, int resident_per_sm = 3);
 
 }  // namespace sd

@@ -368,3 +368,17 @@ def test_fused_deterministic_and_large_window(cuda_lib):
     for x, y in zip(a, b):
         assert torch.equal(x, y)
     _check_fused(sd, workloads.make_case(1, 16, 2, [70001], seed=71), 100.0, "sketch", rows=[(0, h) for h in range(16)])
+
+
+@pytest.mark.parametrize("dist,lens", [("iid", [131072, 20000]), ("needle", [70000, 9000]), ("spec", [50000])])
+def test_fused_fast_path_taken(cuda_lib, dist, lens):
+    """On the paper-shaped workloads the sample bracket holds: no row needs the
+    exact slow path (the fast path is what the bench times)."""
+    sd = cuda_lib
+    case = _dev(workloads.make_case(len(lens), 32, 8, lens, seed=81, dist=dist, n_needles=80))
+    kv, sk = _kv(sd, case)
+    sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE)
+    sd.clear_device_error()
+    sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE)
+    assert sd.read_stats()["fallback_rows"] == 0
+    assert sd.read_device_error() == 0
