@@ -142,26 +142,32 @@ __device__ __forceinline__ void cp_async16_zf(void* dst, const void* src, bool v
 }
 
 // --------------------------------------------------------------------------- 1. sample
-template <int G>
+// One CTA per q-head (grid Hq-of-group x B*Hkv): score the page-strided sample
+// of the row's sequence with the SAME fp32 fma chain as the scan, histogram
+// the keys and read off the two sample order statistics.
 __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
-    int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, int G,
+    float S, int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // [G][CAP]
-  uint32_t* hist = keys + G * CAP;                     // [G][kHistWords] (padded)
-  float* qc = reinterpret_cast<float*>(hist + G * kHistWords);
-  __shared__ int s_bin[G][2];
-  __shared__ uint32_t s_res[G][2];
-  const int bg = blockIdx.x, b = bg / Hkv, g = bg - b * Hkv;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // [CAP]
+  uint32_t* hist = keys + CAP;                         // [kHistWords] (padded)
+  float* qc = reinterpret_cast<float*>(hist + kHistWords);  // [C]
+  __shared__ int s_bin[2];
+  __shared__ uint32_t s_res[2];
+  const int j = blockIdx.x, bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
+  const size_t row = (size_t)b * Hq + g * G + j;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
-  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSampleThreads);
-  for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist[i] = 0;
-  if (tid == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
+  for (int c = tid; c < C; c += kSampleThreads) {
+    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
+    qc[c] = load_q_elem(q, q_dtype, row * kD + ch);
+  }
+  for (int i = tid; i < kHistWords; i += kSampleThreads) hist[i] = 0;
+  if (tid == 0 && j == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
   __syncthreads();
   if (N < 1) return;
   const int k = min(budget_k_dev(N, S, k_fixed), N);
@@ -183,27 +189,22 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
     const int i = tid + u * kSampleThreads;
-    float acc[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) acc[j] = 0.f;
+    float acc = 0.f;
     if (tt[u] >= 0) {
-      sketch_fma8<G>(raw[u], qc, C, acc);
+      sketch_fma8<1>(raw[u], qc, C, &acc);
       if (C > 8) {
         const int t = tt[u];
-        const uint16_t* row = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(row + c0), qc + c0, C, acc);
+        const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rp + c0), qc + c0, C, &acc);
       }
     }
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const uint32_t key = tt[u] >= 0 ? score_key(acc[j]) : 0u;
-      if (i < n_slots) keys[j * CAP + i] = key;
-      // the top-11-bit digit of float keys is heavily shared: aggregate equal
-      // bins within the warp before the shared-memory atomic
-      const uint32_t bin = key ? (key >> 21) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      if (key && (tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[j * kHistWords + hidx(bin)], (uint32_t)__popc(peers));
-    }
+    const uint32_t key = tt[u] >= 0 ? score_key(acc) : 0u;
+    if (i < n_slots) keys[i] = key;
+    // the top-11-bit digit of float keys is heavily shared: aggregate equal
+    // bins within the warp before the shared-memory atomic
+    const uint32_t bin = key ? (key >> 21) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+    if (key && (tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[hidx(bin)], (uint32_t)__popc(peers));
   }
   __syncthreads();
   const int last_sampled = (ns_pages - 1) * spg;
@@ -218,49 +219,42 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     r_hi = (int)floor(mu - kBracketZ * sd);
   }
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
-  // pass 1 (bits 31..21): warp j searches head j for both ranks
-  if (warp < G) {
+  // pass 1 (bits 31..21): warps 0 and 1 search the two ranks
+  if (warp < 2) {
     int bin;
     uint32_t res;
-    warp_find_bin(hist + warp * kHistWords, ra, &bin, &res);
-    if ((tid & 31) == 0) { s_bin[warp][0] = bin; s_res[warp][0] = res; }
-    warp_find_bin(hist + warp * kHistWords, rb, &bin, &res);
-    if ((tid & 31) == 0) { s_bin[warp][1] = bin; s_res[warp][1] = res; }
+    warp_find_bin(hist, warp == 0 ? ra : rb, &bin, &res);
+    if ((tid & 31) == 0) {
+      s_bin[warp] = bin;
+      s_res[warp] = res;
+    }
   }
   __syncthreads();
-  uint32_t tau[G][2];
+  uint32_t tau[2];
 #pragma unroll 1
   for (int w = 0; w < 2; ++w) {
     // pass 2 (bits 20..10) among keys of the pass-1 bin, for rank w
-    for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist[i] = 0;
+    for (int i = tid; i < kHistWords; i += kSampleThreads) hist[i] = 0;
     __syncthreads();
     for (int i = tid; i < n_slots; i += kSampleThreads) {
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const uint32_t key = keys[j * CAP + i];
-        if ((int)(key >> 21) == s_bin[j][w]) atomicAdd(&hist[j * kHistWords + hidx((key >> 10) & 2047)], 1u);
-      }
+      const uint32_t key = keys[i];
+      if ((int)(key >> 21) == s_bin[w]) atomicAdd(&hist[hidx((key >> 10) & 2047)], 1u);
     }
     __syncthreads();
-    if (warp < G) {
+    if (warp == 0) {
       int bin;
       uint32_t res;
-      warp_find_bin(hist + warp * kHistWords, s_res[warp][w], &bin, &res);
-      if ((tid & 31) == 0) s_res[warp][w] = (uint32_t)bin;  // reuse: pass-2 bin
+      warp_find_bin(hist, s_res[w], &bin, &res);
+      if ((tid & 31) == 0) s_res[w] = (uint32_t)bin;  // reuse: pass-2 bin
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const uint32_t pre = ((uint32_t)s_bin[j][w] << 21) | (s_res[j][w] << 10);
-      tau[j][w] = w == 0 ? pre : (pre | 0x3FFu);  // lo: bucket floor; hi: bucket ceiling
-    }
+    const uint32_t pre = ((uint32_t)s_bin[w] << 21) | (s_res[w] << 10);
+    tau[w] = w == 0 ? pre : (pre | 0x3FFu);  // lo: bucket floor; hi: bucket ceiling
   }
-  if (tid < G) {
-    const int j = tid;
-    uint32_t lo = tau[j][0], hi = tau[j][1];
+  if (tid == 0) {
+    uint32_t lo = tau[0], hi = tau[1];
     if (r_lo > n_s) lo = 0u;         // not enough sample mass: every token is a candidate
     if (r_hi < 1) hi = 0xFFFFFFFFu;  // no token is sure
-    const size_t row = (size_t)b * Hq + g * G + j;
     thr[row * 2 + 0] = lo;
     thr[row * 2 + 1] = hi;
   }
@@ -688,11 +682,11 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int BG = geo.B * geo.Hkv;
   cudaError_t e;
   {
-    const size_t smem = sizeof(uint32_t) * G * (kSampleThreads * kSampleSlots + kHistWords) + sizeof(float) * G * C;
-    auto kern = sbs_sample_kernel<G>;
-    set_smem(kern, smem);
-    e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
-                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, w.thr, w.counters);
+    const size_t smem = sizeof(uint32_t) * (kSampleThreads * kSampleSlots + kHistWords) + sizeof(float) * C;
+    set_smem(sbs_sample_kernel, smem);
+    e = launch_pdl(sbs_sample_kernel, dim3(G, BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk,
+                   skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, G, bud.S, bud.k_fixed,
+                   w.thr, w.counters);
     if (e != cudaSuccess) return e;
   }
   {

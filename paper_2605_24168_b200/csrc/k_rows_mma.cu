@@ -79,8 +79,9 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * kR
 
 template <int G>
 struct AttTok {
-  static constexpr int value = G <= 4 ? 16384 : 8192;  // tokens per union-mode CTA (bitmap fits smem)
+  static constexpr int value = 8192;  // tokens per union-mode CTA
 };
+constexpr int kBatchRows = 2048;      // union rows resolved into shared memory at a time
 
 template <int G, bool kDense>
 __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
@@ -89,12 +90,15 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int max_tok,
     void* __restrict__ out, int out_dtype, float* __restrict__ lse_out, int* __restrict__ counters) {
   constexpr int kAtt = AttTok<G>::value;  // union mode: tokens per CTA
+  constexpr int kW = kAtt / 32;
+  constexpr uint32_t kAll = (1u << G) - 1u;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;                                                     // [stages][K | V]
   int* s_pages = reinterpret_cast<int*>(ring + kStagesM * kStageBytesM);          // [max_tok / 16 + 1]
-  constexpr int kW = kAtt / 32;
   uint32_t* bm = reinterpret_cast<uint32_t*>(s_pages + max_tok / 16 + 1);         // [G][kW] head words
   int* upre = reinterpret_cast<int*>(bm + (kDense ? 0 : G * kW));                // [kW + 1]
+  uint16_t* s_tok = reinterpret_cast<uint16_t*>(upre + (kDense ? 0 : kW + 1));   // [kBatchRows] token - T0
+  uint8_t* s_msk = reinterpret_cast<uint8_t*>(s_tok + (kDense ? 0 : kBatchRows));  // [kBatchRows]
   __shared__ int warp_tot[kMmaWarps];
 
   const int bg = blockIdx.y, split = blockIdx.x;
@@ -116,8 +120,7 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     }
   }
   const int N = __ldg(seq_lens + b);
-  // token range of this CTA
-  int T0, T1;
+  int T0, T1;  // token range of this CTA
   if (kDense) {
     int per = (N + splits - 1) / splits;
     per = (per + 15) & ~15;
@@ -129,43 +132,16 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
   }
   const int* pt = page_table + (size_t)b * max_pages;
   for (int i = tid; i < ((T1 - T0 + 15) >> 4); i += kMmaThreads) s_pages[i] = __ldg(pt + (T0 >> 4) + i);
-  int nrows;
   const int nw = (T1 - T0 + 31) >> 5;
+  int total;
   if (kDense) {
-    nrows = T1 - T0;
+    total = T1 - T0;
     __syncthreads();
   } else {
     pdl_wait();  // the selection bitmaps come from sbs_select_kernel
-    nrows = T1 > T0 ? union_prologue<G, kMmaThreads>(fbm, ldw, b * Hq + g * G, T0, T1, bm, upre, warp_tot) : 0;
+    total = T1 > T0 ? union_prologue<G, kMmaThreads>(fbm, ldw, b * Hq + g * G, T0, T1, bm, upre, warp_tot) : 0;
   }
-  const int nst = (nrows + kStageRowsM - 1) / kStageRowsM;
 
-  // row indices ((page * 16 + slot) * Hkv + g) of a stage, resolved once into
-  // a 4-slot shared array by 64 threads; the coalesced cp.async issue then
-  // needs one shared load per row (thread tid always copies chunk tid % 16)
-  __shared__ uint32_t s_ri[4][kStageRowsM];
-  __shared__ uint8_t s_mk[4][kStageRowsM];  // head mask of each stage row
-  constexpr uint32_t kAll = (1u << G) - 1u;
-  auto resolve = [&](int s) {
-    if (tid < kStageRowsM) {
-      const int i = s * kStageRowsM + tid;
-      uint32_t ri = 0xFFFFFFFFu, mk = 0u;
-      if (s < nst && i < nrows) {
-        int tl = i;
-        mk = kAll;
-        if (!kDense) {
-          tl = union_row_token<G>(bm, upre, nw, i);
-          mk = 0u;
-#pragma unroll
-          for (int j = 0; j < G; ++j) mk |= ((bm[j * nw + (tl >> 5)] >> (tl & 31)) & 1u) << j;
-        }
-        const int t = T0 + tl;
-        ri = (uint32_t)(s_pages[(t >> 4) - (T0 >> 4)] * kPS + (t & 15)) * (uint32_t)Hkv + g;
-      }
-      s_ri[s & 3][tid] = ri;
-      s_mk[s & 3][tid] = (uint8_t)mk;
-    }
-  };
   // coalesced cp.async issue: thread tid copies 16-B chunk tid % 16 of rows
   // tid / 16 + 8 i (i < 8) of the K and V blocks; the swizzled destination
   // chunk is the same for all of them ((tid / 16 + 8 i) & 7 == (tid / 16) & 7)
@@ -173,103 +149,136 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
   const uint32_t dsw = (uint32_t)(ir0 * kRowB + ((ic ^ (ir0 & 7)) << 4));
   const char* kpc = kp + ic * 16;
   const char* vpc = vp + ic * 16;
-  auto issue = [&](int s) {
-    if (s < nst) {
-      unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM + dsw;
-      const uint32_t* ris = s_ri[s & 3] + ir0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t ri = ris[8 * i];
-        const bool valid = ri != 0xFFFFFFFFu;
-        const size_t off = valid ? (size_t)ri * kRowB : 0;
-        cp_async16(st + i * 8 * kRowB, kpc + off, valid);
-        cp_async16(st + kStageRowsM * kRowB + i * 8 * kRowB, vpc + off, valid);
-      }
-    }
-    cp_async_commit();
-  };
+  const int p0 = T0 >> 4;
 
   float o[16][4];
 #pragma unroll
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m = -INFINITY, lsum = 0.f;
 
+  // union rows are processed in batches of kBatchRows (one batch unless the
+  // selection is dense); dense mode is a single batch of contiguous rows
+  for (int rb = 0; rb < total; rb += kDense ? total : kBatchRows) {
+    const int nrows = kDense ? total : min(kBatchRows, total - rb);
+    if (!kDense) {
+      // resolve rows [rb, rb + nrows): each thread expands its words
+      __syncthreads();
+      for (int w = tid; w < nw; w += kMmaThreads) {
+        int pos = upre[w];
+        if (pos >= rb + nrows || upre[w + 1] <= rb) continue;
+        uint32_t word = 0;
 #pragma unroll
-  for (int s = 0; s < kStagesM; ++s) resolve(s);
-  __syncthreads();
+        for (int j = 0; j < G; ++j) word |= bm[j * nw + w];
+        while (word) {
+          const int bit = __ffs(word) - 1;
+          word &= word - 1;
+          if (pos >= rb && pos < rb + nrows) {
+            uint32_t mk = 0;
 #pragma unroll
-  for (int s = 0; s < kStagesM - 1; ++s) issue(s);
-  for (int s = 0; s < nst; ++s) {
-    issue(s + kStagesM - 1);
-    cp_async_wait<kStagesM - 1>();
-    __syncthreads();
-    const unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM;
-    const int trow = warp * kTileRows;                 // this warp's tile inside the stage
-    const int rbase = s * kStageRowsM + trow;          // CTA-relative row of the tile
-    if (rbase < nrows) {
-      const uint32_t kb = smem_u32(st) + trow * kRowB;
-      const uint32_t vb = smem_u32(st + kStageRowsM * kRowB) + trow * kRowB;
-      // ---- S = Q K^T for the 16 rows (two n-tiles of 8 rows)
-      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const int r = (lm >> 1) * 8 + lr, c = 2 * kk + (lm & 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + swz(r, c), b0, b1, b2, b3);
-        mma_bf16(sc[0], qa0[kk], qa2[kk], b0, b1);
-        mma_bf16(sc[1], qa0[kk], qa2[kk], b2, b3);
-      }
-      // ---- masked online softmax for head qr (lanes qr >= G are padding)
-      float x[4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int rr = rbase + nt * 8 + qc2 + e;  // CTA-relative row
-          const bool ok = qr < G && ((s_mk[s & 3][trow + nt * 8 + qc2 + e] >> qr) & 1u);
-          x[nt * 2 + e] = ok ? sc[nt][e] * scale_log2 : -INFINITY;
+            for (int j = 0; j < G; ++j) mk |= ((bm[j * nw + w] >> bit) & 1u) << j;
+            s_tok[pos - rb] = (uint16_t)(w * 32 + bit);
+            s_msk[pos - rb] = (uint8_t)mk;
+          }
+          ++pos;
         }
       }
-      float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-      const bool grow = tmax > m;
-      if (__any_sync(0xffffffffu, grow)) {
-        const float mn = grow ? tmax : m;
-        const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
-        lsum *= corr;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          o[i][0] *= corr;
-          o[i][1] *= corr;
-        }
-        m = mn;
-      }
-      float p[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) p[i] = (x[i] == -INFINITY) ? 0.f : exp2f(x[i] - m);
-      lsum += (p[0] + p[1]) + (p[2] + p[3]);
-      // P = P_hi + P_lo (bf16 each) -> A fragments (rows 8..15 zero)
-      const uint32_t ph0 = pack_bf16(p[0], p[1]), ph2 = pack_bf16(p[2], p[3]);
-      const uint32_t pl0 = pack_bf16(p[0] - bf16_round(p[0]), p[1] - bf16_round(p[1]));
-      const uint32_t pl2 = pack_bf16(p[2] - bf16_round(p[2]), p[3] - bf16_round(p[3]));
-      // ---- O += P V over 16 dim-tiles of 8
-#pragma unroll
-      for (int nd = 0; nd < 16; nd += 2) {
-        const int r = (lm & 1) * 8 + lr, c = nd + (lm >> 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + swz(r, c), b0, b1, b2, b3);
-        mma_bf16(o[nd], ph0, ph2, b0, b1);
-        mma_bf16(o[nd], pl0, pl2, b0, b1);
-        mma_bf16(o[nd + 1], ph0, ph2, b2, b3);
-        mma_bf16(o[nd + 1], pl0, pl2, b2, b3);
-      }
+      __syncthreads();
     }
-    resolve(s + kStagesM);  // slot (s + 3) & 3: last read by issue(s - 1) and compute(s - 1)
-    __syncthreads();        // the ring slot may be refilled by the next issue()
+    const int nst = (nrows + kStageRowsM - 1) / kStageRowsM;
+    auto issue = [&](int s) {
+      if (s < nst) {
+        unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM + dsw;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = s * kStageRowsM + ir0 + 8 * i;
+          const bool valid = r < nrows;
+          size_t off = 0;
+          if (valid) {
+            const int tl = kDense ? r : (int)s_tok[r];
+            const int t = T0 + tl;
+            const uint32_t ri = (uint32_t)(s_pages[(t >> 4) - p0] * kPS + (t & 15)) * (uint32_t)Hkv + g;
+            off = (size_t)ri * kRowB;
+          }
+          cp_async16(st + i * 8 * kRowB, kpc + off, valid);
+          cp_async16(st + kStageRowsM * kRowB + i * 8 * kRowB, vpc + off, valid);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < kStagesM - 1; ++s) issue(s);
+    for (int s = 0; s < nst; ++s) {
+      issue(s + kStagesM - 1);
+      cp_async_wait<kStagesM - 1>();
+      __syncthreads();
+      const unsigned char* st = ring + (size_t)(s % kStagesM) * kStageBytesM;
+      const int trow = warp * kTileRows;                 // this warp's tile inside the stage
+      const int rbase = s * kStageRowsM + trow;          // batch-relative row of the tile
+      if (rbase < nrows) {
+        const uint32_t kb = smem_u32(st) + trow * kRowB;
+        const uint32_t vb = smem_u32(st + kStageRowsM * kRowB) + trow * kRowB;
+        // ---- S = Q K^T for the 16 rows (two n-tiles of 8 rows)
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within matrix, matrix id
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int r = (lm >> 1) * 8 + lr, c = 2 * kk + (lm & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + swz(r, c), b0, b1, b2, b3);
+          mma_bf16(sc[0], qa0[kk], qa2[kk], b0, b1);
+          mma_bf16(sc[1], qa0[kk], qa2[kk], b2, b3);
+        }
+        // ---- masked online softmax for head qr (lanes qr >= G are padding)
+        float x[4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int rr = rbase + nt * 8 + qc2 + e;
+            const uint32_t mk = rr < nrows ? (kDense ? kAll : (uint32_t)s_msk[rr]) : 0u;
+            const bool ok = qr < G && ((mk >> qr) & 1u);
+            x[nt * 2 + e] = ok ? sc[nt][e] * scale_log2 : -INFINITY;
+          }
+        }
+        float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        const bool grow = tmax > m;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float mn = grow ? tmax : m;
+          const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+          lsum *= corr;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            o[i][0] *= corr;
+            o[i][1] *= corr;
+          }
+          m = mn;
+        }
+        float p[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p[i] = (x[i] == -INFINITY) ? 0.f : exp2f(x[i] - m);
+        lsum += (p[0] + p[1]) + (p[2] + p[3]);
+        // P = P_hi + P_lo (bf16 each) -> A fragments (rows 8..15 zero)
+        const uint32_t ph0 = pack_bf16(p[0], p[1]), ph2 = pack_bf16(p[2], p[3]);
+        const uint32_t pl0 = pack_bf16(p[0] - bf16_round(p[0]), p[1] - bf16_round(p[1]));
+        const uint32_t pl2 = pack_bf16(p[2] - bf16_round(p[2]), p[3] - bf16_round(p[3]));
+        // ---- O += P V over 16 dim-tiles of 8
+#pragma unroll
+        for (int nd = 0; nd < 16; nd += 2) {
+          const int r = (lm & 1) * 8 + lr, c = nd + (lm >> 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + swz(r, c), b0, b1, b2, b3);
+          mma_bf16(o[nd], ph0, ph2, b0, b1);
+          mma_bf16(o[nd], pl0, pl2, b0, b1);
+          mma_bf16(o[nd + 1], ph0, ph2, b2, b3);
+          mma_bf16(o[nd + 1], pl0, pl2, b2, b3);
+        }
+      }
+      __syncthreads();  // the ring slot may be refilled by the next issue()
+    }
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
   __syncthreads();
   // ---- merge the 4 warps' states per head; lane (qr, qc2) holds head qr, dims 8i + qc2, +1
   lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
@@ -324,17 +333,17 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     __threadfence();
     for (int j = 0; j < G; ++j) {
       const size_t row = (size_t)b * Hq + g * G + j;
-      const float* p = part + row * splits * kPartStride;
+      const float* pp = part + row * splits * kPartStride;
       float M = -INFINITY;
-      for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(p + s2 * kPartStride));
+      for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(pp + s2 * kPartStride));
       float L = 0.f, O = 0.f;
       if (M != -INFINITY) {
         for (int s2 = 0; s2 < splits; ++s2) {
-          const float ms = __ldcg(p + s2 * kPartStride);
+          const float ms = __ldcg(pp + s2 * kPartStride);
           if (ms != -INFINITY) {
             const float c = exp2f(ms - M);
-            L = fmaf(__ldcg(p + s2 * kPartStride + 1), c, L);
-            O = fmaf(__ldcg(p + s2 * kPartStride + 2 + d), c, O);
+            L = fmaf(__ldcg(pp + s2 * kPartStride + 1), c, L);
+            O = fmaf(__ldcg(pp + s2 * kPartStride + 2 + d), c, O);
           }
         }
       }
@@ -354,7 +363,7 @@ cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, con
   if (!kDense) splits = (g.max_seq_len + kAtt - 1) / kAtt;
   const int max_tok = kDense ? (((g.max_seq_len + splits - 1) / splits + 15) & ~15) : kAtt;
   const size_t smem = (size_t)kStagesM * kStageBytesM + sizeof(int) * (max_tok / 16 + 1) +
-                      (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kAtt / 32) + 1)) + 16;
+                      (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kAtt / 32) + 1) + 3 * kBatchRows) + 16;
   static_assert(kStagesM * kStageBytesM >= kMmaWarps * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
   auto kern = attend_rows_mma_kernel<G, kDense>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -400,7 +409,7 @@ cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const voi
 }
 
 int union_att_splits(int G, int max_seq_len) {
-  const int t = G <= 4 ? AttTok<4>::value : AttTok<8>::value;
+  const int t = AttTok<4>::value;
   return (max_seq_len + t - 1) / t;
 }
 
