@@ -50,7 +50,7 @@ constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
 constexpr int kSelNT = 512;
-constexpr int kSelCap = 16384;             // candidates cached per row (keys + tokens: 128 KB)
+constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
 constexpr int kTieCap = 2048;
 
 __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t e) {
@@ -142,35 +142,40 @@ __device__ __forceinline__ void cp_async16_zf(void* dst, const void* src, bool v
 }
 
 // --------------------------------------------------------------------------- 1. sample
-// One CTA per q-head (grid Hq-of-group x B*Hkv): score the page-strided sample
-// of the row's sequence with the SAME fp32 fma chain as the scan, histogram
-// the keys and read off the two sample order statistics.
+// One CTA per q-head (grid G x B*Hkv): score the page-strided sample of the
+// row's sequence with the SAME fp32 fma chain as the scan and histogram the
+// top 14 bits of the keys (16384 bins, fine enough that shared-memory atomics
+// rarely collide).  The bins holding the r_lo-th / r_hi-th largest sample keys
+// give tau_lo = bin floor and tau_hi = bin ceiling (a conservative bracket: a
+// whole bin is ~1/32 of a binade).
+constexpr int kSampleBits = 14;
+constexpr int kSampleBins = 1 << kSampleBits;
 __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, int G,
     float S, int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
+  constexpr int PER = kSampleBins / kSampleThreads;  // bins per thread (32)
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // [CAP]
-  uint32_t* hist = keys + CAP;                         // [kHistWords] (padded)
-  float* qc = reinterpret_cast<float*>(hist + kHistWords);  // [C]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);       // [kSampleBins]
+  float* qc = reinterpret_cast<float*>(hist + kSampleBins);  // [C]
+  __shared__ uint32_t warp_tot[33];
   __shared__ int s_bin[2];
-  __shared__ uint32_t s_res[2];
   const int j = blockIdx.x, bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
   const size_t row = (size_t)b * Hq + g * G + j;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
   for (int c = tid; c < C; c += kSampleThreads) {
     const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
     qc[c] = load_q_elem(q, q_dtype, row * kD + ch);
   }
-  for (int i = tid; i < kHistWords; i += kSampleThreads) hist[i] = 0;
+  for (int i = tid; i < kSampleBins; i += kSampleThreads) hist[i] = 0;
   if (tid == 0 && j == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
+  if (tid < 2) s_bin[tid] = 0;
   __syncthreads();
   if (N < 1) return;
-  const int k = min(budget_k_dev(N, S, k_fixed), N);
   const int npg = (N + 15) >> 4;
   const int cap_pages = CAP >> 4;
   const int spg = (npg + cap_pages - 1) / cap_pages;  // page stride
@@ -186,27 +191,19 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     tt[u] = (i < n_slots && t < N) ? t : -1;
     if (tt[u] >= 0) raw[u] = ldg_nc_v4(sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
+  const int k = min(budget_k_dev(N, S, k_fixed), N);
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
-    const int i = tid + u * kSampleThreads;
+    if (tt[u] < 0) continue;
     float acc = 0.f;
-    if (tt[u] >= 0) {
-      sketch_fma8<1>(raw[u], qc, C, &acc);
-      if (C > 8) {
-        const int t = tt[u];
-        const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rp + c0), qc + c0, C, &acc);
-      }
+    sketch_fma8<1>(raw[u], qc, C, &acc);
+    if (C > 8) {
+      const int t = tt[u];
+      const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+      for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rp + c0), qc + c0, C, &acc);
     }
-    const uint32_t key = tt[u] >= 0 ? score_key(acc) : 0u;
-    if (i < n_slots) keys[i] = key;
-    // the top-11-bit digit of float keys is heavily shared: aggregate equal
-    // bins within the warp before the shared-memory atomic
-    const uint32_t bin = key ? (key >> 21) : 0xFFFFFFFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-    if (key && (tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[hidx(bin)], (uint32_t)__popc(peers));
+    atomicAdd(&hist[score_key(acc) >> (32 - kSampleBits)], 1u);
   }
-  __syncthreads();
   const int last_sampled = (ns_pages - 1) * spg;
   const int n_s = n_slots - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
   int r_lo, r_hi;
@@ -219,40 +216,27 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     r_hi = (int)floor(mu - kBracketZ * sd);
   }
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
-  // pass 1 (bits 31..21): warps 0 and 1 search the two ranks
-  if (warp < 2) {
-    int bin;
-    uint32_t res;
-    warp_find_bin(hist, warp == 0 ? ra : rb, &bin, &res);
-    if ((tid & 31) == 0) {
-      s_bin[warp] = bin;
-      s_res[warp] = res;
-    }
+  __syncthreads();
+  // thread tid owns bins [top - PER + 1, top], top = kSampleBins - 1 - PER * tid
+  const int top = kSampleBins - 1 - PER * tid;
+  uint32_t c[PER], sum = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    c[i] = hist[top - i];
+    sum += c[i];
+  }
+  uint32_t tot;
+  uint32_t above = block_excl_scan<kSampleThreads>(sum, warp_tot, &tot);
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    if (above < ra && above + c[i] >= ra) s_bin[0] = top - i;
+    if (above < rb && above + c[i] >= rb) s_bin[1] = top - i;
+    above += c[i];
   }
   __syncthreads();
-  uint32_t tau[2];
-#pragma unroll 1
-  for (int w = 0; w < 2; ++w) {
-    // pass 2 (bits 20..10) among keys of the pass-1 bin, for rank w
-    for (int i = tid; i < kHistWords; i += kSampleThreads) hist[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < n_slots; i += kSampleThreads) {
-      const uint32_t key = keys[i];
-      if ((int)(key >> 21) == s_bin[w]) atomicAdd(&hist[hidx((key >> 10) & 2047)], 1u);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      int bin;
-      uint32_t res;
-      warp_find_bin(hist, s_res[w], &bin, &res);
-      if ((tid & 31) == 0) s_res[w] = (uint32_t)bin;  // reuse: pass-2 bin
-    }
-    __syncthreads();
-    const uint32_t pre = ((uint32_t)s_bin[w] << 21) | (s_res[w] << 10);
-    tau[w] = w == 0 ? pre : (pre | 0x3FFu);  // lo: bucket floor; hi: bucket ceiling
-  }
   if (tid == 0) {
-    uint32_t lo = tau[0], hi = tau[1];
+    uint32_t lo = (uint32_t)s_bin[0] << (32 - kSampleBits);                 // bin floor
+    uint32_t hi = ((uint32_t)s_bin[1] << (32 - kSampleBits)) | ((1u << (32 - kSampleBits)) - 1u);  // ceiling
     if (r_lo > n_s) lo = 0u;         // not enough sample mass: every token is a candidate
     if (r_hi < 1) hi = 0xFFFFFFFFu;  // no token is sure
     thr[row * 2 + 0] = lo;
@@ -262,27 +246,41 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
 }
 
 // --------------------------------------------------------------------------- 2. scan
-// Candidate entries are written per (b, g, chunk, warp) region of kEntCap
-// slots: ent_tok[...][slot] = token, ent_sc[...][j][slot] = fp32 score of head
-// j (all G heads, for every token that ANY head of the group keeps); ent_cnt
-// holds the (possibly overflowing) count of the region.
-template <int G>
-struct EntCap {
-  static constexpr int value = G <= 4 ? 256 : 512;
-};
-
+// Every token of (b, g) is classified for each of the G q-heads by the bracket:
+//   sure  (key > hi):        its bit is set in the head's selection bitmap fbm
+//                            (one ballot word per 32 tokens; every word of the
+//                            row below N_b is written, so fbm needs no zeroing);
+//   band  (lo <= key <= hi): the token is a union-band entry of the warp's
+//                            region (1024 tokens): ent_tok = token | head mask
+//                            << 24, ent_sc = the G fp32 scores;
+//   below (key < lo):        dropped.
+// ent_cnt[b, g, region] = number of entries (> cap: overflow -> slow path).
 // C8: sketch width 8 (q channels in registers, one 16-B row per token);
 // otherwise a generic C (multiple of 8) with the q channels in shared memory.
+template <int G>
+__device__ __forceinline__ void store_scores(float* dst, const float (&acc)[G]) {
+  if constexpr (G == 1) {
+    dst[0] = acc[0];
+  } else if constexpr (G == 2) {
+    *reinterpret_cast<float2*>(dst) = make_float2(acc[0], acc[1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; j += 4)
+      *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+  }
+}
+
 template <int G, bool C8>
 __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
-    int* __restrict__ ent_cnt, int nch) {
+    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch) {
   constexpr int NW = kScanNT / 32;
-  constexpr int CW = EntCap<G>::value;
+  static_assert(NW == kScanWarps, "one band region per scan warp");
+  constexpr int CW = band_region_cap(G);
   extern __shared__ __align__(128) unsigned char smem[];
-  const int stage_tok = kScanStageTok8 * 8 / C;
+  const int stage_tok = (kScanStageTok8 * 8 / C) & ~31;  // whole bitmap words per stage
   const int stage_bytes = kScanStageTok8 * 16;
   unsigned char* ring = smem;
   float* qc = reinterpret_cast<float*>(ring + (size_t)kScanStages * stage_bytes);  // [G][C]
@@ -290,6 +288,7 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
 
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
+  const int row0 = b * Hq + g * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = __ldg(seq_lens + b);
   const int chunk = blockIdx.x;
@@ -346,24 +345,30 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
       for (int c = 0; c < 8; ++c) qr[j][c] = qc[j * 8 + c];
   }
   pdl_wait();  // the bracket comes from the sample kernel
-  float flo[G];
+  float flo[G], fsure[G];
 #pragma unroll
-  for (int j = 0; j < G; ++j) flo[j] = thresh_lo(__ldg(thr + ((size_t)b * Hq + g * G + j) * 2));
+  for (int j = 0; j < G; ++j) {
+    const uint2 th = __ldg(reinterpret_cast<const uint2*>(thr) + row0 + j);
+    flo[j] = thresh_lo(th.x);
+    fsure[j] = th.y == 0xFFFFFFFFu ? INFINITY : thresh_lo(th.y + 1u);  // key > hi  <=>  s >= fsure
+  }
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t* rtok = ent_tok + reg * CW;
-  float* rsc = ent_sc + reg * G * CW;
-  int wcnt = 0;
+  float* rsc = ent_sc + reg * CW * G;
+  uint32_t* fw = fbm + (size_t)(row0 + (lane < G ? lane : 0)) * ldw;  // lane j < G writes head j's words
+  int wc = 0;
 
   for (int s = 0; s < nst; ++s) {
     issue(s + kScanStages - 1);
     asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
     __syncthreads();
     const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+    const int lim = min(stage_tok, ntok - s * stage_tok);  // valid tokens of this stage
+    const int tbase = t0 + s * stage_tok;                  // first token of the stage
 #pragma unroll 2
     for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
-      const int i = i0 + tid;              // token within the stage
-      const int tl = s * stage_tok + i;    // chunk-relative token
-      const bool valid = i < stage_tok && tl < ntok;
+      const int i = i0 + tid;  // token within the stage
+      const bool valid = i < lim;
       float acc[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) acc[j] = 0.f;
@@ -383,37 +388,52 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
         const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
         for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(src[c0 >> 3], qc + c0, C, acc);
       }
-      bool any = false;
+      // the warp's 32 tokens are one aligned bitmap word (stage_tok, i0 and t0 are multiples of 32)
+      uint32_t my_word = 0, bmask = 0;
 #pragma unroll
-      for (int j = 0; j < G; ++j) any |= acc[j] >= flo[j];
-      any &= valid;
-      const uint32_t bal = __ballot_sync(0xffffffffu, any);
-      const int pos = wcnt + __popc(bal & lt_mask);
-      if (any && pos < CW) {
-        rtok[pos] = (uint32_t)(t0 + tl);
-#pragma unroll
-        for (int j = 0; j < G; ++j) rsc[j * CW + pos] = acc[j];
+      for (int j = 0; j < G; ++j) {
+        const bool sure = valid & (acc[j] >= fsure[j]);
+        const uint32_t sb = __ballot_sync(0xffffffffu, sure);
+        my_word = lane == j ? sb : my_word;
+        bmask |= (uint32_t)(valid & !sure & (acc[j] >= flo[j])) << j;
       }
-      wcnt += __popc(bal);
+      const uint32_t bb = __ballot_sync(0xffffffffu, bmask != 0u);
+      if (bb) {
+        const int pos = wc + __popc(bb & lt_mask);
+        if (bmask && pos < CW) {
+          rtok[pos] = (uint32_t)(tbase + i) | (bmask << 24);
+          store_scores<G>(rsc + (size_t)pos * G, acc);
+        }
+        wc += __popc(bb);
+      }
+      const int wtok = i0 + warp * 32;  // first stage token of the warp
+      if (lane < G && wtok < lim) fw[(tbase + wtok) >> 5] = my_word;
     }
     __syncthreads();  // slot reuse by the next issue()
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (lane == 0) ent_cnt[reg] = wcnt;  // > CW: overflow, the rows of (b, g) take the slow path
+  if (lane == 0) ent_cnt[reg] = wc;
   pdl_launch_dependents();
 }
 
 // --------------------------------------------------------------------------- 3. select (per q-head)
+// One CTA per row: sure = popcount of the row's fbm words (the scan's sure
+// bits), r = k_b - sure; the row's band entries (mask bit j) are gathered into
+// shared memory, the exact r-th largest band key tau found by an adaptive radix
+// select, exact ties at tau resolved lowest token first, and the band winners
+// OR-ed into fbm.  If any check fails (region overflow, band > sel_cap, r < 0
+// or r > band, too many ties) the row is recomputed exactly the slow way into
+// a zeroed fbm row.
 template <int G>
 __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
     int k_fixed, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
-    const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm,
-    int ldw, float* __restrict__ scratch, int ld, int* __restrict__ counts_out, int force_fallback,
-    int* __restrict__ err, int sel_cap) {
-  constexpr int NW = kScanNT / 32;
-  constexpr int CW = EntCap<G>::value;
+    const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm, int ldw,
+    float* __restrict__ scratch, int ld, int* __restrict__ counts_out, int force_fallback, int* __restrict__ err,
+    int sel_cap) {
+  constexpr int NW = kScanWarps;
+  constexpr int CW = band_region_cap(G);
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem);    // [sel_cap]
   uint32_t* toks = keys + sel_cap;                       // [sel_cap]
@@ -427,7 +447,7 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
 
   const int row = blockIdx.x;
   const int Hq = Hkv * G;
-  const int b = row / Hq, j = row - b * Hq - ((row - b * Hq) / G) * G, g = (row - b * Hq) / G;
+  const int b = row / Hq, g = (row - b * Hq) / G, j = row - b * Hq - g * G;
   const int bg = b * Hkv + g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = __ldg(seq_lens + b);
@@ -443,9 +463,7 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
   }
   pdl_wait();
   const int k = N >= 1 ? budget_k_dev(N, S, k_fixed) : 0;
-  const int nw = (max(N, 0) + 31) >> 5;
   uint32_t* fr = fbm + (size_t)row * ldw;
-  for (int w = tid; w < nw; w += kSelNT) fr[w] = 0u;
   if (N < 1 || k > N || k < 1) {
     if (tid == 0) {
       set_error(err, SD_DEVERR_SEQLEN);
@@ -454,159 +472,143 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     return;
   }
   const uint32_t lo = thr[row * 2 + 0], hi = thr[row * 2 + 1];
-  const float flo = thresh_lo(lo);
+  const int nw = (N + 31) >> 5;
   __syncthreads();
-  // ---- this head's candidates from the group's scan entries: region counts
-  // -> prefix (one round trip), then one flat, unrolled pass over all entries
+  // ---- sure count: the scan's bits of this row
+  {
+    int sure = 0;
+    for (int w = tid; w < nw; w += kSelNT) sure += __popc(fr[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
+    if (lane == 0 && sure) atomicAdd(&s_sure, sure);
+  }
+  // ---- this head's band entries: warp per region, all loads of a chunk first
   int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
-  if (nreg > kTieCap - 1) {  // beyond 2M tokens the region table does not fit: exact slow path
+  if (nreg > kTieCap - 1) {  // beyond 2M tokens: exact slow path
     nreg = 0;
     if (tid == 0) s_fb = 1;
   }
-  int* s_roff = reinterpret_cast<int*>(ties);  // reuse: [nreg + 1] region offsets
-  const size_t reg0 = (size_t)bg * nch * NW;
-  int tot = 0;
-  for (int r0 = 0; r0 < nreg; r0 += kSelNT) {
-    const int r = r0 + tid;
-    int c = r < nreg ? ent_cnt[reg0 + r] : 0;
-    if (c > CW) {
-      s_fb = 1;
-      c = 0;
-    }
-    uint32_t all;
-    const uint32_t ex = block_excl_scan<kSelNT>((uint32_t)c, sm.warp_tot, &all);
-    if (r < nreg) s_roff[r] = tot + (int)ex;
-    tot += (int)all;
-  }
-  if (tid == 0) s_roff[nreg] = tot;
-  __syncthreads();
   const uint32_t lt = (1u << lane) - 1u;
-  int sure = 0;
-  // warp per region; all of a region's entries are loaded before any is used
-  constexpr int U = CW / 32;
+  const uint32_t jbit = 1u << (24 + j);
+  const size_t reg0 = (size_t)bg * nch * NW;
+  constexpr int U = CW / 32 < 8 ? CW / 32 : 8;
   for (int r = warp; r < nreg; r += kSelNT / 32) {
-    const int cnt = s_roff[r + 1] - s_roff[r];
     const size_t reg = reg0 + r;
-    const float* rsc = ent_sc + (reg * G + j) * CW;
-    const uint32_t* rtok = ent_tok + reg * CW;
-    float sc[U];
-    uint32_t tk[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = lane + 32 * u;
-      sc[u] = i < cnt ? rsc[i] : -INFINITY;
-      tk[u] = i < cnt ? rtok[i] : 0u;
+    int cnt = ent_cnt[reg];
+    if (cnt > CW) {
+      if (lane == 0) s_fb = 1;
+      cnt = 0;
     }
+    const uint32_t* rtok = ent_tok + reg * CW;
+    const float* rsc = ent_sc + reg * CW * G + j;
+    for (int i0 = 0; i0 < cnt; i0 += 32 * U) {
+      uint32_t tk[U];
+      float sc[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (32 * u >= cnt) break;
-      const bool c = lane + 32 * u < cnt && sc[u] >= flo;
-      const uint32_t bal = __ballot_sync(0xffffffffu, c);
-      if (!bal) continue;
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&s_n, __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (c) {
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + lane + 32 * u;
+        tk[u] = i < cnt ? rtok[i] : 0u;
+        sc[u] = i < cnt ? rsc[(size_t)i * G] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool c = (tk[u] & jbit) != 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, c);
+        if (!bal) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_n, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
         const int p = base + __popc(bal & lt);
-        const uint32_t key = score_key(sc[u]);
-        if (p < sel_cap) {
-          keys[p] = key;
-          toks[p] = tk[u];
+        if (c && p < sel_cap) {
+          keys[p] = score_key(sc[u]);
+          toks[p] = tk[u] & 0x00FFFFFFu;
         }
-        sure += key > hi;
       }
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
-  if (lane == 0 && sure) atomicAdd(&s_sure, sure);
   __syncthreads();
   const int n = s_n;
-  if (tid == 0 && (n > sel_cap || k > n)) s_fb = 1;
+  const int r_need = k - s_sure;
+  if (tid == 0 && (n > sel_cap || r_need < 0 || r_need > n)) s_fb = 1;
   __syncthreads();
-  uint32_t tau = 0xFFFFFFFFu;
-  int cut = INT_MAX;
-  if (!s_fb) {
-    const int r = k - s_sure;
-    if (r < 0) {
-      if (tid == 0) s_fb = 1;  // more than k sure tokens: the bracket missed
-    } else if (r > 0) {
-      // ---- adaptive radix select of the r-th key among band keys (lo <= key <= hi)
-      if (tid == 0) {
-        const uint32_t span = hi - lo;
-        const int bits = span ? 32 - __clz(span) : 1;
-        s_prev = bits;
-        s_shift = bits > 11 ? bits - 11 : 0;
-        s_pre = 0;
-        s_need = (uint32_t)r;
-        s_done = 0;
-      }
-      __syncthreads();
+  if (!s_fb && r_need > 0) {
+    uint32_t tau;
+    int cut = INT_MAX;
+    // ---- adaptive radix select of the r-th largest band key (lo <= key <= hi)
+    if (tid == 0) {
+      const uint32_t span = hi - lo;
+      const int bits = span ? 32 - __clz(span) : 1;
+      s_prev = bits;
+      s_shift = bits > 11 ? bits - 11 : 0;
+      s_pre = 0;
+      s_need = (uint32_t)r_need;
+      s_done = 0;
+    }
+    __syncthreads();
 #pragma unroll 1
-      for (int pass = 0; pass < 3 && !s_done; ++pass) {
-        for (int i = tid; i < kHistWords; i += kSelNT) hist2[i] = 0;
-        __syncthreads();
-        const int sh = s_shift, prev = s_prev;
-        const uint32_t pre = s_pre, dmask = (1u << (prev - sh)) - 1u;
-        for (int i = tid; i < n; i += kSelNT) {
-          const uint32_t key = keys[i];
-          if (key > hi || key < lo) continue;
-          const uint32_t o = key - lo;
-          if ((uint32_t)((uint64_t)o >> prev) != pre) continue;
-          atomicAdd(&hist2[hidx((o >> sh) & dmask)], 1u);
-        }
-        __syncthreads();
-        if (warp == 0) {
-          int bin;
-          uint32_t res;
-          warp_find_bin(hist2, s_need, &bin, &res);
-          if (lane == 0) {
-            s_pre = (uint32_t)(((uint64_t)pre << (prev - sh)) | (uint32_t)bin);
-            s_need = res;
-            s_prev = sh;
-            s_shift = sh > 11 ? sh - 11 : 0;
-            s_done = sh == 0;
-          }
-        }
-        __syncthreads();
-      }
-      tau = lo + s_pre;
-      const uint32_t need = s_need;
-      // ---- exact ties at tau: keep the lowest tokens if not all are needed
-      if (tid == 0) s_ntie = 0;
+    for (int pass = 0; pass < 3 && !s_done; ++pass) {
+      for (int i = tid; i < kHistWords; i += kSelNT) hist2[i] = 0;
       __syncthreads();
+      const int sh = s_shift, prev = s_prev;
+      const uint32_t pre = s_pre, dmask = (1u << (prev - sh)) - 1u;
       for (int i = tid; i < n; i += kSelNT) {
-        if (keys[i] == tau) {
-          const int p = atomicAdd(&s_ntie, 1);
-          if (p < kTieCap) ties[p] = toks[i];
+        const uint32_t o = keys[i] - lo;
+        if ((uint32_t)((uint64_t)o >> prev) != pre) continue;
+        atomicAdd(&hist2[hidx((o >> sh) & dmask)], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        int bin;
+        uint32_t res;
+        warp_find_bin(hist2, s_need, &bin, &res);
+        if (lane == 0) {
+          s_pre = (uint32_t)(((uint64_t)pre << (prev - sh)) | (uint32_t)bin);
+          s_need = res;
+          s_prev = sh;
+          s_shift = sh > 11 ? sh - 11 : 0;
+          s_done = sh == 0;
         }
       }
       __syncthreads();
-      const int ntie = s_ntie;
-      if ((uint32_t)ntie > need) {
-        if (ntie > kTieCap) {
-          if (tid == 0) s_fb = 1;
-        } else {
-          int cap2 = 1;
-          while (cap2 < ntie) cap2 <<= 1;
-          for (int i = ntie + tid; i < cap2; i += kSelNT) ties[i] = 0xFFFFFFFFu;
-          bitonic_sort_smem<kSelNT>(ties, cap2);
-          cut = (int)ties[need - 1];
-        }
+    }
+    tau = lo + s_pre;
+    const uint32_t need = s_need;
+    // ---- exact ties at tau: keep the lowest tokens if not all are needed
+    if (tid == 0) s_ntie = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kSelNT) {
+      if (keys[i] == tau) {
+        const int p = atomicAdd(&s_ntie, 1);
+        if (p < kTieCap) ties[p] = toks[i];
       }
     }
     __syncthreads();
-  }
-  if (!s_fb) {
-    // ---- selection bitmap
-    for (int i = tid; i < n; i += kSelNT) {
-      const uint32_t key = keys[i];
-      const int t = (int)toks[i];
-      if (key > hi || key > tau || (key == tau && t <= cut)) atomicOr(&fr[t >> 5], 1u << (t & 31));
+    const int ntie = s_ntie;
+    if ((uint32_t)ntie > need) {
+      if (ntie > kTieCap) {
+        if (tid == 0) s_fb = 1;
+      } else {
+        int cap2 = 1;
+        while (cap2 < ntie) cap2 <<= 1;
+        for (int i = ntie + tid; i < cap2; i += kSelNT) ties[i] = 0xFFFFFFFFu;
+        bitonic_sort_smem<kSelNT>(ties, cap2);
+        cut = (int)ties[need - 1];
+      }
     }
-  } else {
-    // ---- exact slow path for this row: scores -> scratch, radix select, bitmap
+    __syncthreads();
+    if (!s_fb) {
+      // ---- band winners into the bitmap
+      for (int i = tid; i < n; i += kSelNT) {
+        const uint32_t key = keys[i];
+        const int t = (int)toks[i];
+        if (key > tau || (key == tau && t <= cut)) atomicOr(&fr[t >> 5], 1u << (t & 31));
+      }
+    }
+  }
+  if (s_fb) {
+    // ---- exact slow path for this row: zero the row, scores -> scratch, radix select, bitmap
     if (tid == 0 && err) atomicAdd(err + 1, 1);  // statistics word: fallback rows
+    for (int w = tid; w < nw; w += kSelNT) fr[w] = 0u;
     float* sr = scratch + (size_t)row * ld;
     for (int t = tid; t < N; t += kSelNT) {
       const uint16_t* rowp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
@@ -674,6 +676,21 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// Shared-memory band capacity of the select kernel.  The band holds the tokens
+// between the two sample order statistics: about (2 z sigma + 2) / f tokens
+// (sigma = sqrt(k f (1 - f)), f = sample fraction) plus the two edge bins;
+// sized at 1.5x that + 2048, within [4096, kSelCap] (4 select CTAs per SM at
+// the low end, 1 at the high end).
+int band_capacity(int max_seq_len, Budget bud) {
+  const double N = std::max(1, max_seq_len);
+  const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N) : std::ceil(N / bud.S);
+  const double f = std::min(1.0, (double)(kSampleThreads * kSampleSlots) / N);
+  const double sig = std::sqrt(k * f * (1.0 - f));
+  const double band = (2.0 * kBracketZ * sig + 2.0) / f;
+  const int cap = (int)std::min<double>(kSelCap, std::max(4096.0, 1.5 * band + 2048.0));
+  return (cap + 255) & ~255;
+}
+
 template <int G>
 cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch& skc, const void* q, Budget bud,
                          const SbsBuffers& w, cudaStream_t st) {
@@ -682,45 +699,34 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int BG = geo.B * geo.Hkv;
   cudaError_t e;
   {
-    const size_t smem = sizeof(uint32_t) * (kSampleThreads * kSampleSlots + kHistWords) + sizeof(float) * C;
+    const size_t smem = sizeof(uint32_t) * kSampleBins + sizeof(float) * C;
     set_smem(sbs_sample_kernel, smem);
     e = launch_pdl(sbs_sample_kernel, dim3(G, BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk,
                    skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, G, bud.S, bud.k_fixed,
                    w.thr, w.counters);
     if (e != cudaSuccess) return e;
   }
+  const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
   {
     const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 + sizeof(float) * G * C +
                         sizeof(int) * (kRangeTok / 16);
-    const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
     dim3 grid(nch, BG);
-    if (C == 8) {
-      auto kern = sbs_scan_kernel<G, true>;
-      set_smem(kern, smem);
-      e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
-                     reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
-                     geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch);
-    } else {
-      auto kern = sbs_scan_kernel<G, false>;
-      set_smem(kern, smem);
-      e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
-                     reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
-                     geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch);
-    }
+    auto kern = C == 8 ? sbs_scan_kernel<G, true> : sbs_scan_kernel<G, false>;
+    set_smem(kern, smem);
+    e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
+                   reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
+                   geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch);
     if (e != cudaSuccess) return e;
   }
   {
-    // candidate capacity: 2 k_max + 4096 (bracket width at the default sample), <= kSelCap
-    const int kmax = bud.k_fixed > 0 ? bud.k_fixed : (int)ceil((double)geo.max_seq_len / (double)bud.S);
-    const int sel_cap = std::min(kSelCap, ((2 * kmax + 4096) + 255) & ~255);
+    const int sel_cap = band_capacity(geo.max_seq_len, bud);
     const size_t smem = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
-    const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
     auto kern = sbs_select_kernel<G>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(geo.B * geo.Hq), dim3(kSelNT), smem, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, (const uint32_t*)w.thr,
-                   (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch, w.fbm, w.ldw,
-                   w.scratch, w.ld, w.counts_out, w.force_fallback, w.err, sel_cap);
+                   (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld, w.counts_out,
+                   w.force_fallback, w.err, sel_cap);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

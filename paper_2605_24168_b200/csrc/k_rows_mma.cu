@@ -32,7 +32,6 @@ constexpr int kTileRows = 16;
 constexpr int kStageRowsM = kMmaWarps * kTileRows;   // 64 rows per stage
 constexpr int kRowB = 256;                           // one bf16 K or V row
 constexpr int kStageBytesM = kStageRowsM * 2 * kRowB;  // 32 KB (K block then V block)
-constexpr int kStagesM = 3;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
   const uint32_t d = smem_u32(dst);
@@ -83,6 +82,13 @@ struct AttTok {
 };
 constexpr int kBatchRows = 2048;      // union rows resolved into shared memory at a time
 
+// ring depth: 3 stages (2 in flight) for dense; 2 stages for union mode so
+// that 3 CTAs fit per SM and their per-range prologues overlap
+template <bool kDense>
+struct RingStages {
+  static constexpr int value = kDense ? 3 : 2;
+};
+
 template <int G, bool kDense>
 __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
@@ -92,6 +98,7 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
   constexpr int kAtt = AttTok<G>::value;  // union mode: tokens per CTA
   constexpr int kW = kAtt / 32;
   constexpr uint32_t kAll = (1u << G) - 1u;
+  constexpr int kStagesM = RingStages<kDense>::value;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;                                                     // [stages][K | V]
   int* s_pages = reinterpret_cast<int*>(ring + kStagesM * kStageBytesM);          // [max_tok / 16 + 1]
@@ -362,9 +369,10 @@ cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, con
   constexpr int kAtt = AttTok<G>::value;
   if (!kDense) splits = (g.max_seq_len + kAtt - 1) / kAtt;
   const int max_tok = kDense ? (((g.max_seq_len + splits - 1) / splits + 15) & ~15) : kAtt;
+  constexpr int kStagesM = RingStages<kDense>::value;
   const size_t smem = (size_t)kStagesM * kStageBytesM + sizeof(int) * (max_tok / 16 + 1) +
                       (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kAtt / 32) + 1) + 3 * kBatchRows) + 16;
-  static_assert(kStagesM * kStageBytesM >= kMmaWarps * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
+  static_assert(2 * kStageBytesM >= kMmaWarps * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
   auto kern = attend_rows_mma_kernel<G, kDense>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};

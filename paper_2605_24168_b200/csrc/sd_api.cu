@@ -37,8 +37,8 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
     L.thr = off;
     off = align256(off + rows * 2 * sizeof(uint32_t));
     const int G = Hq / Hkv;
-    const size_t nreg = (size_t)B * Hkv * L.nrange * 8;
-    const size_t cap = G <= 4 ? 256 : 512;  // EntCap<G> in k_fused.cu
+    const size_t nreg = (size_t)B * Hkv * L.nrange * kScanWarps;
+    const size_t cap = band_region_cap(G);
     L.ent_tok = off;
     off = align256(off + nreg * cap * sizeof(uint32_t));
     L.ent_sc = off;

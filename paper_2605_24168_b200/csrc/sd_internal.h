@@ -14,6 +14,9 @@ constexpr int kHeadDim = 128;       // the only compiled head_dim
 constexpr int kPageSize = 16;       // the only compiled page size
 constexpr int kMaxSplits = 64;      // split-k partial slots per (b, h) row (dense / list paths)
 constexpr int kPartStride = 128 + 2;  // {m (log2 domain), l, o[128] unnormalised}
+constexpr int kScanWarps = 8;         // warps per scan CTA = band regions per 8192-token range
+// union-band entries per (b, g, region of 1024 tokens): 128 per q-head of the group
+constexpr int band_region_cap(int G) { return G >= 8 ? 1024 : 128 * G; }
 
 // Resolved, validated arguments passed from the C-ABI layer to launchers.
 struct Geo {
@@ -40,9 +43,9 @@ struct WsLayout {
   // fused path (sample-bracket select, sd_sbs.cuh)
   int nrange = 0, ldw = 0;
   size_t thr = 0;            // uint32 [B*Hq][2]
-  size_t ent_tok = 0;        // uint32 [B*Hkv][nrange][8 warps][cap]
-  size_t ent_sc = 0;         // float  [B*Hkv][nrange][8 warps][G][cap]
-  size_t ent_cnt = 0;        // int32  [B*Hkv][nrange][8 warps]
+  size_t ent_tok = 0;        // uint32 token | head mask << 24  [B*Hkv][nrange * 8][cap]  (union band)
+  size_t ent_sc = 0;         // float scores [B*Hkv][nrange * 8][cap][G]
+  size_t ent_cnt = 0;        // int32 [B*Hkv][nrange * 8] entry counts (> cap: overflow)
   size_t fbm = 0;            // uint32 [B*Hq][ldw] selection bitmap
   size_t ctr = 0;            // int32 [B*Hkv] last-CTA merge counters (zero between calls)
   size_t total = 0;
@@ -87,7 +90,7 @@ int choose_splits(int rows, int work_per_row, int min_per_split);
 // ---- fused sample-bracket select (k_fused.cu) -------------------------------
 struct SbsBuffers {
   uint32_t* thr;
-  uint32_t* ent_tok;             // scan candidate entries (see k_fused.cu)
+  uint32_t* ent_tok;             // scan union-band entries (see sd_sbs.cuh)
   float* ent_sc;
   int* ent_cnt;
   uint32_t* fbm;
