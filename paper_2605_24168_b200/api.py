@@ -318,6 +318,6 @@ def _ws_bytes_budget(g, bud, max_seq_len, k_max):
 
 
 # Kernel launches enqueued by one sd_sparse_decode_fused call in sketch mode
-# (sample, scan, select, attend_rows with the split merge folded in, bf16 KV) -
+# with bf16 KV (sample, scan, select, persistent union attend, split merge) -
 # keep in sync with csrc/sd_api.cu.
-LAUNCHES_PER_FUSED = 4
+LAUNCHES_PER_FUSED = 5

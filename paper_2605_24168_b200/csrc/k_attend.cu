@@ -242,21 +242,41 @@ __global__ void __launch_bounds__(kAttThreads) dense_kernel(
 __global__ void __launch_bounds__(128) merge_parts_kernel(const float* __restrict__ part, int splits,
                                                           void* __restrict__ out, int out_dtype,
                                                           float* __restrict__ lse) {
-  const int row = blockIdx.x, d = threadIdx.x;
+  // splits <= blockDim.x * 4 (host-checked); all loads of a phase are independent
+  __shared__ float s_c[4 * 128];
+  __shared__ float s_red[2][4];
+  const int row = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  pdl_wait();  // no-op unless launched as a programmatic dependent
   const float* p = part + (size_t)row * splits * kPartStride;
-  float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, p[s * kPartStride]);
-  float L = 0.f, O = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < splits; ++s) {
-      const float ms = p[s * kPartStride];
-      if (ms != -INFINITY) {
-        const float c = exp2f(ms - M);
-        L = fmaf(p[s * kPartStride + 1], c, L);
-        O = fmaf(p[s * kPartStride + 2 + d], c, O);
-      }
-    }
+  float mv[4], lv[4], M = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int s = d + 128 * k;
+    mv[k] = s < splits ? __ldcg(p + s * kPartStride) : -INFINITY;
+    lv[k] = s < splits ? __ldcg(p + s * kPartStride + 1) : 0.f;
+    M = fmaxf(M, mv[k]);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  if (lane == 0) s_red[0][warp] = M;
+  __syncthreads();
+  M = fmaxf(fmaxf(s_red[0][0], s_red[0][1]), fmaxf(s_red[0][2], s_red[0][3]));
+  float L = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int s = d + 128 * k;
+    const float c = (M == -INFINITY || mv[k] == -INFINITY) ? 0.f : exp2f(mv[k] - M);
+    if (s < splits) s_c[s] = c;
+    L = fmaf(lv[k], c, L);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  if (lane == 0) s_red[1][warp] = L;
+  __syncthreads();
+  L = (s_red[1][0] + s_red[1][1]) + (s_red[1][2] + s_red[1][3]);
+  float O = 0.f;
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) O = fmaf(__ldcg(p + s * kPartStride + 2 + d), s_c[s], O);
   store_out(out, out_dtype, (size_t)row * kD + d, L > 0.f ? O / L : 0.f);
   if (lse && d == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
 }
@@ -340,8 +360,24 @@ cudaError_t launch_dense(const Geo& g, const sd_paged_kv& kv, const void* q, flo
 
 cudaError_t launch_merge_parts(const float* part, int rows, int splits, void* out,
                                int out_dtype, float* lse, cudaStream_t st) {
+  if (splits > 4 * 128) return cudaErrorInvalidValue;  // merge_parts_kernel bound
   merge_parts_kernel<<<rows, 128, 0, st>>>(part, splits, out, out_dtype, lse);
   return cudaGetLastError();
+}
+
+cudaError_t launch_merge_parts_pdl(const float* part, int rows, int splits, void* out, int out_dtype, float* lse,
+                                   cudaStream_t st) {
+  if (splits > 4 * 128) return cudaErrorInvalidValue;  // merge_parts_kernel bound
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, merge_parts_kernel, part, splits, out, out_dtype, lse);
 }
 
 cudaError_t launch_lse_merge(int parts, int rows, const float* part_o, const float* part_lse,

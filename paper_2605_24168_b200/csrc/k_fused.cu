@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   }
   for (int i = tid; i < kSampleBins; i += kSampleThreads) hist[i] = 0;
   if (tid == 0 && j == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
+  if (tid == 0 && j == 0 && bg == 0) counters[gridDim.y] = 0;  // and the work counter
   if (tid < 2) s_bin[tid] = 0;
   __syncthreads();
   if (N < 1) return;

@@ -23,7 +23,7 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
   L.part = off;
   off = align256(off + rows * (size_t)L.part_splits * kPartStride * sizeof(float));
   L.ctr = off;
-  off = align256(off + (size_t)B * Hkv * sizeof(int));
+  off = align256(off + ((size_t)B * Hkv + 1) * sizeof(int));
   if (with_budget) {
     L.ld = (max_seq_len + 63) & ~63;
     L.ldw = L.ld / 32;
@@ -309,7 +309,14 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
   w.err = err;
   SD_CUDA(launch_sbs_select(g, *kv, *sketch, q, bud, w, st));
   if (g.kv_dtype == SD_BF16)
-    return cuda_status(launch_attend_rows_mma(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
+  {
+    // union gather-attend variant (A/B switch for measurements): pk (default,
+    // persistent, + split merge kernel), rows (one CTA per range, merge folded)
+    const char* v = getenv("SD_UNION_ATTEND");
+    if (v && !strcmp(v, "rows"))
+      return cuda_status(launch_attend_rows_mma(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
+    return cuda_status(launch_attend_union_pk(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
+  }
   const int splits = L.nrange;
   SD_CUDA(launch_attend_rows(g, *kv, q, w.fbm, w.ldw, scale, part, splits, st));
   return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));

@@ -47,7 +47,7 @@ struct WsLayout {
   size_t ent_sc = 0;         // float scores [B*Hkv][nrange * 8][cap][G]
   size_t ent_cnt = 0;        // int32 [B*Hkv][nrange * 8] entry counts (> cap: overflow)
   size_t fbm = 0;            // uint32 [B*Hq][ldw] selection bitmap
-  size_t ctr = 0;            // int32 [B*Hkv] last-CTA merge counters (zero between calls)
+  size_t ctr = 0;            // int32 [B*Hkv + 1] last-CTA merge counters + work counter (zero between calls)
   size_t total = 0;
 };
 
@@ -80,6 +80,10 @@ cudaError_t launch_dense(const Geo& g, const sd_paged_kv& kv, const void* q, flo
 // Combine `splits` unnormalised partials per row into out / lse.
 cudaError_t launch_merge_parts(const float* part, int rows, int splits, void* out,
                                int out_dtype, float* lse, cudaStream_t st);
+
+// Same, launched as a programmatic dependent of the preceding kernel (PDL).
+cudaError_t launch_merge_parts_pdl(const float* part, int rows, int splits, void* out,
+                                   int out_dtype, float* lse, cudaStream_t st);
 
 // Combine normalised (o, lse) parts (cross-GPU partials).
 cudaError_t launch_lse_merge(int parts, int rows, const float* part_o, const float* part_lse,
@@ -120,6 +124,10 @@ cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const vo
                                    cudaStream_t st);
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
                                   int splits, void* out, float* lse, int* counters, cudaStream_t st);
+// persistent variant (k_attend_pk.cu); the split partials are merged by a
+// following merge_parts_kernel (PDL)
+cudaError_t launch_attend_union_pk(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
+                                   float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st);
 int union_att_splits(int G, int max_seq_len);
 int choose_row_splits(int groups, int rows_per_group, int resident_per_sm = 3);
 
