@@ -142,39 +142,77 @@ __device__ __forceinline__ void cp_async16_zf(void* dst, const void* src, bool v
 }
 
 // --------------------------------------------------------------------------- 1. sample
-// One CTA per q-head (grid G x B*Hkv): score the page-strided sample of the
-// row's sequence with the SAME fp32 fma chain as the scan and histogram the
-// top 14 bits of the keys (16384 bins, fine enough that shared-memory atomics
-// rarely collide).  The bins holding the r_lo-th / r_hi-th largest sample keys
-// give tau_lo = bin floor and tau_hi = bin ceiling (a conservative bracket: a
-// whole bin is ~1/32 of a binade).
-constexpr int kSampleBits = 14;
-constexpr int kSampleBins = 1 << kSampleBits;
+// One CTA per (b, g) for its G q-heads (the sampled sketch rows are loaded once):
+// score the deterministic page-strided sample (every spg-th page, <= 4096
+// tokens) with the SAME fp32 fma chain as the scan; the scores stay in
+// registers.  The r_lo-th / r_hi-th largest sample keys of each head are found
+// in two histogram passes (11 + 8 key bits): tau_lo = floor of the 19-bit bin
+// holding the r_lo-th key, tau_hi = ceiling of the bin holding the r_hi-th
+// (a bin is 1/4096 of a binade, so the bracket is set by the sample
+// statistics, not by the binning).
+constexpr int kSampleBits1 = 11, kSampleBits2 = 8;
+constexpr int kSampleSh1 = 32 - kSampleBits1, kSampleSh2 = kSampleSh1 - kSampleBits2;  // 21, 13
+
+// bin of the r-th largest element of a 256-bin histogram (one warp); (bin, residual)
+__device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, int* bin_out, uint32_t* res_out) {
+  const int lane = threadIdx.x & 31;
+  const int top = 255 - 8 * lane;  // lane owns bins [top - 7, top]
+  uint32_t c[8], sum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    c[i] = h[top - i];
+    sum += c[i];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t above = incl - sum;
+  const uint32_t who = __ballot_sync(0xffffffffu, above < r && incl >= r);
+  const int src = who ? __ffs(who) - 1 : 31;
+  int bin = top - 7;
+  uint32_t res = 1;
+  bool found = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (!found && above + c[i] >= r) {
+      bin = top - i;
+      res = r - above;
+      found = true;
+    }
+    above += c[i];
+  }
+  *bin_out = __shfl_sync(0xffffffffu, bin, src);
+  *res_out = __shfl_sync(0xffffffffu, res, src);
+}
+
+template <int G>
 __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, int G,
-    float S, int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
+    int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
-  constexpr int PER = kSampleBins / kSampleThreads;  // bins per thread (32)
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);       // [kSampleBins]
-  float* qc = reinterpret_cast<float*>(hist + kSampleBins);  // [C]
-  __shared__ uint32_t warp_tot[33];
-  __shared__ int s_bin[2];
-  const int j = blockIdx.x, bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
+  uint32_t* hist1 = reinterpret_cast<uint32_t*>(smem);  // [G][kHistWords] padded 2048-bin
+  uint32_t* hist2 = hist1 + G * kHistWords;              // [G][2][256]
+  float* qc = reinterpret_cast<float*>(hist2 + G * 512);  // [G][C]
+  __shared__ int s_bin1[G][2];
+  __shared__ uint32_t s_res[G][2];
+  __shared__ uint32_t s_lohi[G][2];
+  const int bg = blockIdx.x, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
-  const size_t row = (size_t)b * Hq + g * G + j;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
-  for (int c = tid; c < C; c += kSampleThreads) {
-    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
-    qc[c] = load_q_elem(q, q_dtype, row * kD + ch);
+  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSampleThreads);
+  for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist1[i] = 0;
+  for (int i = tid; i < G * 512; i += kSampleThreads) hist2[i] = 0;
+  if (tid == 0) {
+    counters[bg] = 0;                   // re-arm the gather-attend merge counter of (b, g)
+    if (bg == 0) counters[gridDim.x] = 0;  // and the work counter
   }
-  for (int i = tid; i < kSampleBins; i += kSampleThreads) hist[i] = 0;
-  if (tid == 0 && j == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
-  if (tid == 0 && j == 0 && bg == 0) counters[gridDim.y] = 0;  // and the work counter
-  if (tid < 2) s_bin[tid] = 0;
   __syncthreads();
   if (N < 1) return;
   const int npg = (N + 15) >> 4;
@@ -193,17 +231,25 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     if (tt[u] >= 0) raw[u] = ldg_nc_v4(sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
   const int k = min(budget_k_dev(N, S, k_fixed), N);
+  uint32_t key[kSampleSlots][G];
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
-    if (tt[u] < 0) continue;
-    float acc = 0.f;
-    sketch_fma8<1>(raw[u], qc, C, &acc);
-    if (C > 8) {
-      const int t = tt[u];
-      const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-      for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rp + c0), qc + c0, C, &acc);
+    float acc[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) acc[j] = 0.f;
+    if (tt[u] >= 0) {
+      sketch_fma8<G>(raw[u], qc, C, acc);
+      if (C > 8) {
+        const int t = tt[u];
+        const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(rp + c0), qc + c0, C, acc);
+      }
     }
-    atomicAdd(&hist[score_key(acc) >> (32 - kSampleBits)], 1u);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      key[u][j] = score_key(acc[j]);
+      if (tt[u] >= 0) atomicAdd(&hist1[j * kHistWords + hidx(key[u][j] >> kSampleSh1)], 1u);
+    }
   }
   const int last_sampled = (ns_pages - 1) * spg;
   const int n_s = n_slots - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
@@ -218,28 +264,47 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   }
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
   __syncthreads();
-  // thread tid owns bins [top - PER + 1, top], top = kSampleBins - 1 - PER * tid
-  const int top = kSampleBins - 1 - PER * tid;
-  uint32_t c[PER], sum = 0;
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    c[i] = hist[top - i];
-    sum += c[i];
-  }
-  uint32_t tot;
-  uint32_t above = block_excl_scan<kSampleThreads>(sum, warp_tot, &tot);
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    if (above < ra && above + c[i] >= ra) s_bin[0] = top - i;
-    if (above < rb && above + c[i] >= rb) s_bin[1] = top - i;
-    above += c[i];
+  // level 1: warp 2 j + e finds the 11-bit bin of rank (ra, rb)[e] for head j
+  if (warp < 2 * G) {
+    const int j = warp >> 1, e = warp & 1;
+    int bin;
+    uint32_t res;
+    warp_find_bin(hist1 + j * kHistWords, e ? rb : ra, &bin, &res);
+    if (lane == 0) {
+      s_bin1[j][e] = bin;
+      s_res[j][e] = res;
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    uint32_t lo = (uint32_t)s_bin[0] << (32 - kSampleBits);                 // bin floor
-    uint32_t hi = ((uint32_t)s_bin[1] << (32 - kSampleBits)) | ((1u << (32 - kSampleBits)) - 1u);  // ceiling
+  // level 2: the next 8 key bits inside the two bins of each head
+#pragma unroll
+  for (int u = 0; u < kSampleSlots; ++u) {
+    if (tt[u] < 0) continue;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int b1 = (int)(key[u][j] >> kSampleSh1);
+      const uint32_t b2 = (key[u][j] >> kSampleSh2) & 255u;
+      if (b1 == s_bin1[j][0]) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
+      if (b1 == s_bin1[j][1]) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+    }
+  }
+  __syncthreads();
+  if (warp < 2 * G) {
+    const int j = warp >> 1, e = warp & 1;
+    int bin;
+    uint32_t res;
+    warp_find_bin256(hist2 + (j * 2 + e) * 256, s_res[j][e], &bin, &res);
+    if (lane == 0) {
+      const uint32_t pre = ((uint32_t)s_bin1[j][e] << kSampleSh1) | ((uint32_t)bin << kSampleSh2);
+      s_lohi[j][e] = e ? (pre | ((1u << kSampleSh2) - 1u)) : pre;  // hi: bin ceiling, lo: bin floor
+    }
+  }
+  __syncthreads();
+  if (tid < G) {
+    uint32_t lo = s_lohi[tid][0], hi = s_lohi[tid][1];
     if (r_lo > n_s) lo = 0u;         // not enough sample mass: every token is a candidate
     if (r_hi < 1) hi = 0xFFFFFFFFu;  // no token is sure
+    const size_t row = (size_t)b * Hq + g * G + tid;
     thr[row * 2 + 0] = lo;
     thr[row * 2 + 1] = hi;
   }
@@ -272,7 +337,7 @@ __device__ __forceinline__ void store_scores(float* dst, const float (&acc)[G]) 
 }
 
 template <int G, bool C8>
-__global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
+__global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
@@ -308,18 +373,22 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
   __syncthreads();
   const int nst = (ntok + stage_tok - 1) / stage_tok;
   const int cpt = C >> 3;  // 16-B chunks per token
+  // C8: thread tid copies tokens tid + 256 u of a stage: page (tid >> 4) + 16 u
+  // of the stage's 64, slot tid & 15 (fixed per thread)
+  const char* tb = skb + ((size_t)g * kPS + (tid & 15)) * 16;
+  const uint32_t page_bytes = (uint32_t)Hkv * kPS * 16;
+  int slot_in = 0;  // ring slot of the next issue
   auto issue = [&](int s) {
     if (s < nst) {
-      unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+      unsigned char* st = ring + (size_t)slot_in * stage_bytes;
       if (C8) {
-        // one 16-B chunk per token; thread tid copies tokens tid + 256 u
-        const char* gb = skb + ((size_t)g * kPS) * 16;
 #pragma unroll
         for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
           const int ti = tid + u * kScanNT;
           const int i = s * kScanStageTok8 + ti;  // chunk-relative token
           const bool valid = i < ntok;
-          const char* src = valid ? gb + ((size_t)s_pages[i >> 4] * Hkv * kPS + (i & 15)) * 16 : skb;
+          const uint32_t pg = (uint32_t)s_pages[(s * kScanStageTok8 >> 4) + (ti >> 4)];
+          const char* src = valid ? tb + (size_t)pg * page_bytes : skb;
           cp_async16_zf(st + (size_t)ti * 16, src, valid);
         }
       } else {
@@ -332,6 +401,7 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
           cp_async16_zf(st + (size_t)qd * 16, src, valid);
         }
       }
+      slot_in = slot_in + 1 == kScanStages ? 0 : slot_in + 1;
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -358,15 +428,17 @@ __global__ void __launch_bounds__(kScanNT) sbs_scan_kernel(
   float* rsc = ent_sc + reg * CW * G;
   uint32_t* fw = fbm + (size_t)(row0 + (lane < G ? lane : 0)) * ldw;  // lane j < G writes head j's words
   int wc = 0;
+  int slot_out = 0;  // ring slot of the stage being scored
 
   for (int s = 0; s < nst; ++s) {
     issue(s + kScanStages - 1);
     asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
     __syncthreads();
-    const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+    const unsigned char* st = ring + (size_t)slot_out * stage_bytes;
+    slot_out = slot_out + 1 == kScanStages ? 0 : slot_out + 1;
     const int lim = min(stage_tok, ntok - s * stage_tok);  // valid tokens of this stage
     const int tbase = t0 + s * stage_tok;                  // first token of the stage
-#pragma unroll 2
+#pragma unroll 4
     for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
       const int i = i0 + tid;  // token within the stage
       const bool valid = i < lim;
@@ -700,11 +772,11 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int BG = geo.B * geo.Hkv;
   cudaError_t e;
   {
-    const size_t smem = sizeof(uint32_t) * kSampleBins + sizeof(float) * C;
-    set_smem(sbs_sample_kernel, smem);
-    e = launch_pdl(sbs_sample_kernel, dim3(G, BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk,
-                   skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, G, bud.S, bud.k_fixed,
-                   w.thr, w.counters);
+    const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C;
+    auto kern = sbs_sample_kernel<G>;
+    set_smem(kern, smem);
+    e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
+                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, w.thr, w.counters);
     if (e != cudaSuccess) return e;
   }
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
