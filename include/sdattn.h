@@ -212,6 +212,20 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
                                  int32_t k_max_out, void* ws, size_t ws_bytes,
                                  sd_stream stream);
 
+/* Measurement helper (not for production use): sd_sparse_decode_fused in
+ * sketch mode with a CUDA event recorded after each of its kernels; it
+ * synchronizes `stream` and writes the kernels' durations in milliseconds to
+ * phase_ms[0..n_phases): [0] sample, [1] scan, [2] select, [3] gather-attend,
+ * [4] split merge (entries past 5, or of phases the path does not have, are
+ * -1).  The events serialise the kernels (no programmatic-dependent-launch
+ * overlap), so the sum exceeds the untimed call's duration.  Returns
+ * SD_ERR_INVALID_ARG if sketch == NULL. */
+sd_status sd_sparse_decode_fused_timed(const sd_geometry* geom, const sd_paged_kv* kv,
+                                       const sd_sketch* sketch, const void* q,
+                                       const sd_budget* budget, float scale, void* out,
+                                       float* lse, void* ws, size_t ws_bytes,
+                                       sd_stream stream, float* phase_ms, int32_t n_phases);
+
 /* ---- A7: dense decode (P:59 dense regime, speedup context) -------
  * Full softmax over all N_b rows; each K/V row is loaded once per GQA group. */
 sd_status sd_dense_decode(const sd_geometry* geom, const sd_paged_kv* kv,

@@ -68,6 +68,8 @@ _PROTOS = {
                                         c_vp, c_vp, c_size, c_vp]),
     "sd_sparse_decode_fused": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_f32, c_vp, c_vp,
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_vp]),
+    "sd_sparse_decode_fused_timed": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_f32, c_vp,
+                                             c_vp, c_vp, c_size, c_vp, P(c_f32), c_i32]),
     "sd_dense_decode": (c_i32, [P(Geometry), P(PagedKV), c_vp, c_f32, c_vp, c_vp, c_vp, c_size, c_vp]),
     "sd_lse_merge": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "sd_seqshard_local_topk": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_vp, c_i32, c_vp,

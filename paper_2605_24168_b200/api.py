@@ -244,6 +244,29 @@ def sparse_decode_fused(q, kv: KVCache, sketch: Optional[SketchCache], S: float 
     return out, lse
 
 
+FUSED_PHASES = ("sample", "scan", "select", "attend", "merge")
+
+
+def sparse_decode_fused_timed(q, kv: KVCache, sketch: SketchCache, S: float = 50.0, k_fixed: int = 0,
+                              scale: Optional[float] = None, out=None, lse=None, stream=None):
+    """Measurement helper: the fused step with CUDA events between its kernels
+    (serialised; synchronizes) -> (out, lse, {phase: ms})."""
+    g = geometry(q, kv, None)
+    bud = make_budget(S, k_fixed)
+    scale = scale if scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    out = out if out is not None else torch.empty(q.shape, dtype=q.dtype, device=q.device)
+    lse = lse if lse is not None else torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
+    kvs, sk = kv.c_struct(), sketch.c_struct()
+    ws = workspace(workspace_size(g, bud, kv.max_seq_len), q.device, stream)
+    p, n = _ws_ptr(ws)
+    ms = (ctypes.c_float * len(FUSED_PHASES))()
+    _check(C.load().sd_sparse_decode_fused_timed(ctypes.byref(g), ctypes.byref(kvs), ctypes.byref(sk), _ptr(q),
+                                                 ctypes.byref(bud), float(scale), _ptr(out), _ptr(lse), p, n,
+                                                 _stream(stream), ms, len(FUSED_PHASES)),
+           "sd_sparse_decode_fused_timed")
+    return out, lse, {k: float(v) for k, v in zip(FUSED_PHASES, ms)}
+
+
 def dense_decode(q, kv: KVCache, scale: Optional[float] = None, out_dtype=None, out=None, lse=None, stream=None):
     """A7: full softmax over all N_b rows -> (out, lse)."""
     g = geometry(q, kv, out_dtype)

@@ -416,7 +416,8 @@ int g_pk_sms = 0;
 
 template <int G>
 cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                        float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st) {
+                        float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st,
+                        cudaEvent_t ev_attend) {
   const int splits = (g.max_seq_len + kPkItemTok - 1) / kPkItemTok;
   const int n_items = splits * g.B * g.Hkv;
   const size_t smem = sizeof(PkSmem<G>);
@@ -445,18 +446,20 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
                             kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
                             n_items, out, g.out_dtype, lse);
   if (e != cudaSuccess) return e;
+  if (ev_attend) cudaEventRecord(ev_attend, st);
   return launch_merge_parts_pdl(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st);
 }
 
 }  // namespace
 
 cudaError_t launch_attend_union_pk(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                                   float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st) {
+                                   float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st,
+                                   cudaEvent_t ev_attend) {
   switch (g.G) {
-    case 1: return launch_pk_t<1>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st);
-    case 2: return launch_pk_t<2>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st);
-    case 4: return launch_pk_t<4>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st);
-    case 8: return launch_pk_t<8>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st);
+    case 1: return launch_pk_t<1>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st, ev_attend);
+    case 2: return launch_pk_t<2>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st, ev_attend);
+    case 4: return launch_pk_t<4>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st, ev_attend);
+    case 8: return launch_pk_t<8>(g, kv, q, fbm, ldw, scale, part, out, lse, counters, st, ev_attend);
   }
   return cudaErrorInvalidValue;
 }

@@ -778,6 +778,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, w.thr, w.counters);
     if (e != cudaSuccess) return e;
+    if (w.ev) cudaEventRecord(w.ev[0], st);
   }
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
   {
@@ -790,6 +791,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
                    geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch);
     if (e != cudaSuccess) return e;
+    if (w.ev) cudaEventRecord(w.ev[1], st);
   }
   {
     const int sel_cap = band_capacity(geo.max_seq_len, bud);
@@ -801,6 +803,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
                    (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld, w.counts_out,
                    w.force_fallback, w.err, sel_cap);
     if (e != cudaSuccess) return e;
+    if (w.ev) cudaEventRecord(w.ev[2], st);
   }
   return cudaSuccess;
 }

@@ -259,10 +259,14 @@ sd_status sd_sparse_gather_attend(const sd_geometry* geom, const sd_paged_kv* kv
   return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
 }
 
-sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
-                                 const void* q, const sd_budget* budget, float scale, void* out, float* lse,
-                                 int32_t* idx_out, int32_t* counts_out, int32_t k_max_out, void* ws,
-                                 size_t ws_bytes, sd_stream stream) {
+namespace {
+
+// The fused step; ev (nullable) = 6 events: [0] before the first kernel, then
+// one after each of sample, scan, select, attend, merge (bf16 sketch path).
+sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch, const void* q,
+                     const sd_budget* budget, float scale, void* out, float* lse, int32_t* idx_out,
+                     int32_t* counts_out, int32_t k_max_out, void* ws, size_t ws_bytes, sd_stream stream,
+                     cudaEvent_t* ev) {
   SD_TRY(check_kv(kv, true));
   Geo g;
   SD_TRY(check_geom(geom, kv->max_seq_len, &g));
@@ -307,19 +311,62 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
   const char* ff = getenv("SD_FORCE_FALLBACK");
   w.force_fallback = (ff && ff[0] == '1') ? 1 : 0;
   w.err = err;
+  w.ev = ev ? ev + 1 : nullptr;
+  if (ev) cudaEventRecord(ev[0], st);
   SD_CUDA(launch_sbs_select(g, *kv, *sketch, q, bud, w, st));
   if (g.kv_dtype == SD_BF16)
   {
     // union gather-attend variant (A/B switch for measurements): pk (default,
     // persistent, + split merge kernel), rows (one CTA per range, merge folded)
     const char* v = getenv("SD_UNION_ATTEND");
-    if (v && !strcmp(v, "rows"))
-      return cuda_status(launch_attend_rows_mma(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
-    return cuda_status(launch_attend_union_pk(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
+    if (v && !strcmp(v, "rows")) {
+      SD_CUDA(launch_attend_rows_mma(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
+      if (ev) {
+        cudaEventRecord(ev[4], st);
+        cudaEventRecord(ev[5], st);
+      }
+      return cuda_status(cudaGetLastError());
+    }
+    SD_CUDA(launch_attend_union_pk(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st,
+                                   ev ? ev[4] : nullptr));
+    if (ev) cudaEventRecord(ev[5], st);
+    return cuda_status(cudaGetLastError());
   }
   const int splits = L.nrange;
   SD_CUDA(launch_attend_rows(g, *kv, q, w.fbm, w.ldw, scale, part, splits, st));
-  return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
+  if (ev) cudaEventRecord(ev[4], st);
+  SD_CUDA(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
+  if (ev) cudaEventRecord(ev[5], st);
+  return cuda_status(cudaGetLastError());
+}
+
+}  // namespace
+
+sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
+                                 const void* q, const sd_budget* budget, float scale, void* out, float* lse,
+                                 int32_t* idx_out, int32_t* counts_out, int32_t k_max_out, void* ws,
+                                 size_t ws_bytes, sd_stream stream) {
+  return fused_impl(geom, kv, sketch, q, budget, scale, out, lse, idx_out, counts_out, k_max_out, ws, ws_bytes,
+                    stream, nullptr);
+}
+
+sd_status sd_sparse_decode_fused_timed(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
+                                       const void* q, const sd_budget* budget, float scale, void* out, float* lse,
+                                       void* ws, size_t ws_bytes, sd_stream stream, float* phase_ms,
+                                       int32_t n_phases) {
+  if (!sketch || !phase_ms || n_phases < 1) return SD_ERR_INVALID_ARG;
+  cudaEvent_t ev[6];
+  for (int i = 0; i < 6; ++i)
+    if (cudaEventCreate(&ev[i]) != cudaSuccess) return SD_ERR_CUDA;
+  sd_status s = fused_impl(geom, kv, sketch, q, budget, scale, out, lse, nullptr, nullptr, 0, ws, ws_bytes, stream,
+                           ev);
+  if (s == SD_OK && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) s = SD_ERR_CUDA;
+  for (int i = 0; i < n_phases; ++i) {
+    phase_ms[i] = -1.f;
+    if (s == SD_OK && i < 5) cudaEventElapsedTime(&phase_ms[i], ev[i], ev[i + 1]);
+  }
+  for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+  return s;
 }
 
 sd_status sd_dense_decode(const sd_geometry* geom, const sd_paged_kv* kv, const void* q, float scale,

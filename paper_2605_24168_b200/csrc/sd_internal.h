@@ -107,6 +107,7 @@ struct SbsBuffers {
   int k_max_out;
   int force_fallback;
   int* err;
+  cudaEvent_t* ev = nullptr;     // optional: recorded after sample, scan, select (measurement)
 };
 
 cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
@@ -127,7 +128,8 @@ cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const voi
 // persistent variant (k_attend_pk.cu); the split partials are merged by a
 // following merge_parts_kernel (PDL)
 cudaError_t launch_attend_union_pk(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                                   float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st);
+                                   float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st,
+                                   cudaEvent_t ev_attend = nullptr);
 int union_att_splits(int G, int max_seq_len);
 int choose_row_splits(int groups, int rows_per_group, int resident_per_sm = 3);
 
