@@ -49,6 +49,8 @@ constexpr int kSampleSlots = 8;            // sample tokens per thread (cap 4096
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
+constexpr int kScanMaxWords = kScanStageTok8 / 32;  // bitmap words per stage (C = 8: 32)
+constexpr int kScanCandCap = kScanStageTok8 / 8;    // candidates per warp per stage (<= its tokens)
 constexpr int kSelNT = 512;
 constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
 constexpr int kTieCap = 2048;
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
     int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* hist1 = reinterpret_cast<uint32_t*>(smem);  // [G][kHistWords] padded 2048-bin
   uint32_t* hist2 = hist1 + G * kHistWords;              // [G][2][256]
   float* qc = reinterpret_cast<float*>(hist2 + G * 512);  // [G][C]
@@ -336,6 +338,26 @@ __device__ __forceinline__ void store_scores(float* dst, const float (&acc)[G]) 
   }
 }
 
+template <int G>
+__device__ __forceinline__ void load_scores(float (&sc)[G], const float* src) {
+  if constexpr (G == 1) {
+    sc[0] = src[0];
+  } else if constexpr (G == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(src);
+    sc[0] = v.x;
+    sc[1] = v.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; j += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(src + j);
+      sc[j] = v.x;
+      sc[j + 1] = v.y;
+      sc[j + 2] = v.z;
+      sc[j + 3] = v.w;
+    }
+  }
+}
+
 template <int G, bool C8>
 __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
@@ -351,6 +373,9 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   unsigned char* ring = smem;
   float* qc = reinterpret_cast<float*>(ring + (size_t)kScanStages * stage_bytes);  // [G][C]
   int* s_pages = reinterpret_cast<int*>(qc + G * C);                                // [kRangeTok / 16]
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pages + kRangeTok / 16);        // [G][kScanMaxWords]
+  float* c_sc_all = reinterpret_cast<float*>(s_words + G * kScanMaxWords);          // [NW][kScanCandCap][G]
+  uint16_t* c_tok_all = reinterpret_cast<uint16_t*>(c_sc_all + NW * G * kScanCandCap);  // [NW][kScanCandCap]
 
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
@@ -382,14 +407,22 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     if (s < nst) {
       unsigned char* st = ring + (size_t)slot_in * stage_bytes;
       if (C8) {
+        const int* sp = s_pages + (s * kScanStageTok8 >> 4) + (tid >> 4);
+        if ((s + 1) * kScanStageTok8 <= ntok) {  // full stage: plain copies
 #pragma unroll
-        for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
-          const int ti = tid + u * kScanNT;
-          const int i = s * kScanStageTok8 + ti;  // chunk-relative token
-          const bool valid = i < ntok;
-          const uint32_t pg = (uint32_t)s_pages[(s * kScanStageTok8 >> 4) + (ti >> 4)];
-          const char* src = valid ? tb + (size_t)pg * page_bytes : skb;
-          cp_async16_zf(st + (size_t)ti * 16, src, valid);
+          for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
+            const uint32_t d = smem_u32(st + (size_t)(tid + u * kScanNT) * 16);
+            const char* src = tb + (size_t)(uint32_t)sp[u * (kScanNT >> 4)] * page_bytes;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+          }
+        } else {  // the range's tail: rows past the end are zero-filled
+#pragma unroll
+          for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
+            const int ti = tid + u * kScanNT;
+            const bool valid = s * kScanStageTok8 + ti < ntok;
+            const char* src = valid ? tb + (size_t)(uint32_t)sp[u * (kScanNT >> 4)] * page_bytes : skb;
+            cp_async16_zf(st + (size_t)ti * 16, src, valid);
+          }
         }
       } else {
         const int nq = stage_tok * cpt;
@@ -426,7 +459,12 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t* rtok = ent_tok + reg * CW;
   float* rsc = ent_sc + reg * CW * G;
-  uint32_t* fw = fbm + (size_t)(row0 + (lane < G ? lane : 0)) * ldw;  // lane j < G writes head j's words
+  float* c_sc = c_sc_all + warp * G * kScanCandCap;      // this warp's candidates of the stage ([p][G])
+  uint16_t* c_tok = c_tok_all + warp * kScanCandCap;
+  // bitmap words owned per stage: lane < G * nown handles head own_j, word own_w
+  const int nown = C8 ? kScanStageTok8 / kScanNT : (stage_tok + kScanNT - 1) / kScanNT;
+  const int own_j = lane / nown, own_w = (lane - own_j * nown) * NW + warp;
+  uint32_t* fw = fbm + (size_t)(row0 + (own_j < G ? own_j : 0)) * ldw;
   int wc = 0;
   int slot_out = 0;  // ring slot of the stage being scored
 
@@ -438,6 +476,10 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     slot_out = slot_out + 1 == kScanStages ? 0 : slot_out + 1;
     const int lim = min(stage_tok, ntok - s * stage_tok);  // valid tokens of this stage
     const int tbase = t0 + s * stage_tok;                  // first token of the stage
+    // this warp owns bitmap words w + 8 q of the stage (the tokens it scores)
+    if (lane < G * nown) s_words[own_j * kScanMaxWords + own_w] = 0u;
+    // ---- phase 1: score every token; keep the candidates (key >= lo for some head)
+    int wn = 0;
 #pragma unroll 4
     for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
       const int i = i0 + tid;  // token within the stage
@@ -461,27 +503,47 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
         for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(src[c0 >> 3], qc + c0, C, acc);
       }
-      // the warp's 32 tokens are one aligned bitmap word (stage_tok, i0 and t0 are multiples of 32)
-      uint32_t my_word = 0, bmask = 0;
+      bool cand = false;
+#pragma unroll
+      for (int j = 0; j < G; ++j) cand |= acc[j] >= flo[j];
+      cand &= valid;
+      const uint32_t cb = __ballot_sync(0xffffffffu, cand);
+      if (cand) {
+        const int p = wn + __popc(cb & lt_mask);
+        c_tok[p] = (uint16_t)i;
+        store_scores<G>(c_sc + p * G, acc);
+      }
+      wn += __popc(cb);
+    }
+    __syncwarp();
+    // ---- phase 2: classify the candidates, one per lane: sure bits into the
+    // stage words (shared-memory atomics), band tokens into the region
+    for (int c0 = 0; c0 < wn; c0 += 32) {
+      const int ci = c0 + lane;
+      const bool have = ci < wn;
+      const int i = have ? (int)c_tok[ci] : 0;
+      float sc[G];
+      uint32_t bm = 0;
+      load_scores<G>(sc, c_sc + (have ? ci : 0) * G);
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const bool sure = valid & (acc[j] >= fsure[j]);
-        const uint32_t sb = __ballot_sync(0xffffffffu, sure);
-        my_word = lane == j ? sb : my_word;
-        bmask |= (uint32_t)(valid & !sure & (acc[j] >= flo[j])) << j;
+        if (!have) sc[j] = -INFINITY;
+        if (sc[j] >= fsure[j]) atomicOr(&s_words[j * kScanMaxWords + (i >> 5)], 1u << (i & 31));
+        else if (sc[j] >= flo[j]) bm |= 1u << j;
       }
-      const uint32_t bb = __ballot_sync(0xffffffffu, bmask != 0u);
+      const uint32_t bb = __ballot_sync(0xffffffffu, bm != 0u);
       if (bb) {
         const int pos = wc + __popc(bb & lt_mask);
-        if (bmask && pos < CW) {
-          rtok[pos] = (uint32_t)(tbase + i) | (bmask << 24);
-          store_scores<G>(rsc + (size_t)pos * G, acc);
+        if (bm && pos < CW) {
+          rtok[pos] = (uint32_t)(tbase + i) | (bm << 24);
+          store_scores<G>(rsc + (size_t)pos * G, sc);
         }
         wc += __popc(bb);
       }
-      const int wtok = i0 + warp * 32;  // first stage token of the warp
-      if (lane < G && wtok < lim) fw[(tbase + wtok) >> 5] = my_word;
     }
+    __syncwarp();
+    // ---- this warp's words of the stage -> the G rows' selection bitmaps
+    if (lane < G * nown && own_w * 32 < lim) fw[(tbase >> 5) + own_w] = s_words[own_j * kScanMaxWords + own_w];
     __syncthreads();  // slot reuse by the next issue()
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -507,7 +569,7 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     int sel_cap) {
   constexpr int NW = kScanWarps;
   constexpr int CW = band_region_cap(G);
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem);    // [sel_cap]
   uint32_t* toks = keys + sel_cap;                       // [sel_cap]
   uint32_t* ties = toks + sel_cap;                       // [kTieCap]
@@ -783,7 +845,8 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
   {
     const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 + sizeof(float) * G * C +
-                        sizeof(int) * (kRangeTok / 16);
+                        sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * kScanMaxWords +
+                        (sizeof(float) * G + sizeof(uint16_t)) * kScanWarps * kScanCandCap;
     dim3 grid(nch, BG);
     auto kern = C == 8 ? sbs_scan_kernel<G, true> : sbs_scan_kernel<G, false>;
     set_smem(kern, smem);
