@@ -626,38 +626,60 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t jbit = 1u << (24 + j);
   const size_t reg0 = (size_t)bg * nch * NW;
-  constexpr int U = CW / 32 < 8 ? CW / 32 : 8;
-  for (int r = warp; r < nreg; r += kSelNT / 32) {
-    const size_t reg = reg0 + r;
-    int cnt = ent_cnt[reg];
-    if (cnt > CW) {
-      if (lane == 0) s_fb = 1;
-      cnt = 0;
+  // region counts -> shared memory in one coalesced pass (overflow: slow path)
+  int* s_cnt = reinterpret_cast<int*>(ties);  // reuse: [nreg]
+  for (int r = tid; r < nreg; r += kSelNT) {
+    int c = ent_cnt[reg0 + r];
+    if (c > CW) {
+      s_fb = 1;
+      c = 0;
     }
-    const uint32_t* rtok = ent_tok + reg * CW;
-    const float* rsc = ent_sc + reg * CW * G + j;
-    for (int i0 = 0; i0 < cnt; i0 += 32 * U) {
-      uint32_t tk[U];
-      float sc[U];
+    s_cnt[r] = c;
+  }
+  __syncthreads();
+  // warp per region with RQ regions in flight: entries lane + 32 u (u < UQ) of
+  // each are loaded before any is used; longer regions finish in a tail loop
+  constexpr int RQ = 4, UQ = 4;
+  auto keep = [&](uint32_t tk, float scv) {
+    const bool c = (tk & jbit) != 0u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, c);
+    if (!bal) return;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&s_n, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const int p = base + __popc(bal & lt);
+    if (c && p < sel_cap) {
+      keys[p] = score_key(scv);
+      toks[p] = tk & 0x00FFFFFFu;
+    }
+  };
+  for (int rb = warp; rb < nreg; rb += (kSelNT / 32) * RQ) {
+    uint32_t tk[RQ][UQ];
+    float sc[RQ][UQ];
+    int cnt[RQ];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + lane + 32 * u;
-        tk[u] = i < cnt ? rtok[i] : 0u;
-        sc[u] = i < cnt ? rsc[(size_t)i * G] : 0.f;
+    for (int qq = 0; qq < RQ; ++qq) {
+      const int r = rb + (kSelNT / 32) * qq;
+      cnt[qq] = r < nreg ? s_cnt[r] : 0;
+      const uint32_t* rtok = ent_tok + (reg0 + r) * CW;
+      const float* rsc = ent_sc + (reg0 + r) * CW * G + j;
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) {
+        const int i = lane + 32 * u;
+        tk[qq][u] = i < cnt[qq] ? rtok[i] : 0u;
+        sc[qq][u] = i < cnt[qq] ? rsc[(size_t)i * G] : 0.f;
       }
+    }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool c = (tk[u] & jbit) != 0u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, c);
-        if (!bal) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&s_n, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const int p = base + __popc(bal & lt);
-        if (c && p < sel_cap) {
-          keys[p] = score_key(sc[u]);
-          toks[p] = tk[u] & 0x00FFFFFFu;
-        }
+    for (int qq = 0; qq < RQ; ++qq)
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) keep(tk[qq][u], sc[qq][u]);
+    for (int qq = 0; qq < RQ; ++qq) {
+      const int r = rb + (kSelNT / 32) * qq;
+      for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
+        const int i = i0 + lane;
+        const bool in = i < cnt[qq];
+        keep(in ? ent_tok[(reg0 + r) * CW + i] : 0u, in ? ent_sc[((reg0 + r) * CW + i) * G + j] : 0.f);
       }
     }
   }
