@@ -233,6 +233,36 @@ def test_fused_sketch_matches_oracle(cuda_lib, dist):
     _check_fused(cuda_lib, case, 50.0, "sketch")
 
 
+@pytest.mark.parametrize("G,Hkv", [(1, 4), (2, 3), (8, 2)])
+@pytest.mark.parametrize("S", [2.0, 10.0, 50.0])
+def test_fused_sketch_group_sizes_and_sparsity(cuda_lib, G, Hkv, S):
+    """Every GQA group size of the persistent union attend, including low
+    sparsity (items with several 1024-row work units) and ragged lengths that
+    end inside a page, a bitmap word and an 8192-token item."""
+    lens = [20000, 8193, 37]
+    case = workloads.make_case(len(lens), G * Hkv, Hkv, lens, seed=101 + G, dist="spec")
+    _check_fused(cuda_lib, case, S, "sketch")
+
+
+def test_fused_sketch_fp32_kv(cuda_lib):
+    """fp32 KV with a sketch: the CUDA-core union attend + split merge path."""
+    lens = [9000, 300]
+    case = workloads.make_case(len(lens), 8, 2, lens, seed=61, dtype=torch.float32)
+    _check_fused(cuda_lib, case, 20.0, "sketch")
+
+
+def test_fused_timed_matches_untimed(cuda_lib):
+    """sd_sparse_decode_fused_timed: same output as the untimed call, five
+    non-negative kernel durations."""
+    sd = cuda_lib
+    case = _dev(workloads.make_case(2, 32, 8, [20000, 5000], seed=67, dist="needle", n_needles=16))
+    kv, sk = _kv(sd, case)
+    o1, l1 = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE)
+    o2, l2, ph = sd.api.sparse_decode_fused_timed(case.q, kv, sk, S=50.0, scale=SCALE)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert set(ph) == set(sd.api.FUSED_PHASES) and all(v >= 0 for v in ph.values()), ph
+
+
 @pytest.mark.parametrize("S", [1.0, 2.0, 10.0, 100.0, 500.0])
 def test_fused_exact_mode_sparsity_sweep(cuda_lib, S):
     lens = [3, 257, 6000]
