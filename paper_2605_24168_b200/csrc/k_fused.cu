@@ -9,21 +9,20 @@
 //     sample of each sequence (every spg-th page, <= 4096 tokens) for the G
 //     q-heads of the KV head and take two sample order statistics per head,
 //       r_lo = ceil(k f + z sqrt(k f (1-f)) + 1),  r_hi = floor(k f - z sqrt(...))
-//     (f = sample fraction, z = 4).  Their 22-bit key buckets give tau_lo
-//     (bucket floor) <= tau_hi (bucket ceiling) such that, with overwhelming
-//     probability, #{key >= tau_lo} >= k_b >= #{key > tau_hi}.  When the sample
-//     is the whole row (f = 1) the bracket is the bucket of the exact k-th key.
+//     (f = sample fraction, z = 4), located with an 11 + 8 bit histogram.  The
+//     floor / ceiling of their 19-bit key bins give tau_lo <= tau_hi such that,
+//     with overwhelming probability, #{key >= tau_lo} >= k_b >= #{key > tau_hi}.
+//     When the sample is the whole row the bracket is the bin of the exact k-th key.
 //  2. sbs_scan_kernel (grid chunks x B*Hkv): the bandwidth-bound pass.  The
 //     chunk's sketch rows (16 B per token and KV head) stream through a
 //     3-stage cp.async ring; each token's G scores are formed with the same
-//     fp32 fma chain as sd_sparse_index_score (packed FFMA2) and compared with
-//     tau_lo.  The only output is one ballot word per head and 32 tokens: the
-//     candidate bitmap cbm (~3% of bits set).
-//  3. sbs_select_kernel (grid B*Hq, one CTA per q-head): the row's candidate
-//     tokens are listed in token order from cbm, their exact scores recomputed
-//     (same fp32 code), r = k_b - #{key > tau_hi}, the exact r-th key tau of
-//     the band by an adaptive radix select, exact ties at tau kept lowest
-//     token first; the result is written as the selection bitmap fbm.  If a
+//     fp32 fma chain as sd_sparse_index_score (packed FFMA2).  Tokens above
+//     tau_hi ("sure") go straight into the selection bitmap fbm; tokens inside
+//     the bracket ("band") are appended with their G scores to the warp's region.
+//  3. sbs_select_kernel (grid B*Hq, one CTA per q-head): sure = popcount of the
+//     row's bitmap, r = k_b - sure; the exact r-th largest band key tau is found
+//     by an adaptive radix select over the head's band entries, exact ties at
+//     tau kept lowest token first, and the band winners OR-ed into fbm.  If a
 //     check fails (bracket missed, too many candidates, too many ties) the CTA
 //     computes the row exactly the slow way (all scores, same fp32 code, radix
 //     select, ordered emission) into the same fbm.  Identical result either way.

@@ -3,9 +3,11 @@
 // (k_rows_mma.cu, k_rows.cu).
 //
 // Per q-row (b, h) with N_b tokens:
-//   thr[row] = {lo, hi}                sample bracket keys   (sbs_sample_kernel)
-//   cbm[row][t / 32] bit t = key(s_t) >= lo   candidate bitmap  (sbs_scan_kernel)
-//   fbm[row][t / 32] bit t = t is in the exact top-k_b          (sbs_select_kernel)
+//   thr[row] = {lo, hi}      sample bracket keys                       (sbs_sample_kernel)
+//   fbm[row][t / 32] bit t = key(s_t) > hi after sbs_scan_kernel (sure tokens),
+//                          = t is in the exact top-k_b after sbs_select_kernel
+//   band entries (lo <= key <= hi for some head of the group): per (b, g,
+//   8192-token chunk, scan warp) region, token | head mask << 24 and G scores
 // where key() is the order-preserving uint32 map of the fp32 indexer score
 // (sd_common.cuh score_key).  A gather-attend CTA owning tokens [T0, T1) of
 // (b, g) ORs the G heads' fbm words of its range into the ascending GQA union
