@@ -116,8 +116,15 @@ typedef struct {
 /* Sparsity budget ("each query-head attends to 1/S fraction of total
  * tokens").  k_b = max(1, ceil(N_b / sparsity)) evaluated in double
  * precision, or k_fixed when k_fixed > 0 (absolute form; k_fixed > N_b
- * is a device error SD_DEVERR_SEQLEN).  n_sink/n_local/heavy_fraction are the
- * Sink+Local+heavy scaffold of P:462-463 (reserved: must be 0 in this version). */
+ * is a device error SD_DEVERR_SEQLEN).
+ * Sink + Local + heavy (NEXT-1), active when any of
+ * n_sink, n_local, heavy_fraction is non-zero: with lo = min(n_sink, N_b),
+ * hi = max(lo, N_b - min(n_local, N_b)), mid = hi - lo, the row keeps every
+ * sink [0, lo), every local [hi, N_b) and the top-kh of the middle [lo, hi),
+ * kh = min(k_fixed, mid) if k_fixed > 0, else min(mid, floor(heavy_fraction *
+ * mid + 1/2)); sparsity is ignored.  AC8: N = 20000, 128 + 128, 0.20 -> 4205
+ * rows.  n_sink, n_local >= 0 and 0 <= heavy_fraction <= 1, else INVALID_ARG;
+ * the sequence-shard entries return UNSUPPORTED for such budgets. */
 typedef struct {
   float sparsity;
   int32_t k_fixed;
@@ -130,8 +137,9 @@ typedef struct {
 const char* sd_status_str(sd_status s);
 const char* sd_version(void);
 
-/* k for one sequence of N tokens.  INVALID_ARG if S < 1,
- * N < 1, or k_fixed > N. */
+/* Rows kept for one sequence of N tokens (with sinks / locals the
+ * total sinks + locals + heavy).  INVALID_ARG if S < 1, N < 1, or
+ * k_fixed > N in the plain form, or an invalid NEXT-1 field. */
 sd_status sd_budget_k(const sd_budget* budget, int32_t N, int32_t* k);
 
 /* Workspace bytes sufficient for EVERY entry point below called with this

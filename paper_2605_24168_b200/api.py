@@ -101,9 +101,12 @@ def make_budget(S: float = 1.0, k_fixed: int = 0, n_sink: int = 0, n_local: int 
     return C.Budget(float(S), int(k_fixed), int(n_sink), int(n_local), float(heavy_fraction))
 
 
-def budget_k(S: float, N: int, k_fixed: int = 0) -> int:
+def budget_k(S: float, N: int, k_fixed: int = 0, n_sink: int = 0, n_local: int = 0,
+             heavy_fraction: float = 0.0) -> int:
+    """Rows kept for one sequence of N tokens: max(1, ceil(N/S)) or k_fixed; with
+    sinks / locals / a heavy fraction (NEXT-1) sinks + locals + the middle's heavy budget."""
     k = C.c_i32()
-    b = make_budget(S, k_fixed)
+    b = make_budget(S, k_fixed, n_sink, n_local, heavy_fraction)
     _check(C.load().sd_budget_k(ctypes.byref(b), int(N), ctypes.byref(k)), "sd_budget_k")
     return k.value
 
@@ -184,12 +187,13 @@ def sparse_index_score(q, kv: KVCache, sketch: Optional[SketchCache] = None, sco
 
 
 def topk_select(scores, seq_lens, max_seq_len: int, S: float = 1.0, k_fixed: int = 0, num_kv_heads=None,
-                k_max: Optional[int] = None, stream=None):
+                k_max: Optional[int] = None, stream=None, n_sink: int = 0, n_local: int = 0,
+                heavy_fraction: float = 0.0):
     """A3: (idx int32 [B][Hq][k_max] ascending, counts int32 [B][Hq])."""
     B, Hq, ld = scores.shape
-    bud = make_budget(S, k_fixed)
+    bud = make_budget(S, k_fixed, n_sink, n_local, heavy_fraction)
     if k_max is None:
-        k_max = budget_k(S, max_seq_len, k_fixed)
+        k_max = max(1, budget_k(S, max_seq_len, k_fixed, n_sink, n_local, heavy_fraction))
     Hkv = num_kv_heads or Hq
     g = C.Geometry(B, Hq, Hkv, 128, 16, (max_seq_len + 15) // 16, C.SD_BF16, C.SD_BF16, C.SD_BF16)
     idx = torch.full((B, Hq, k_max), -1, dtype=torch.int32, device=scores.device)
@@ -220,15 +224,17 @@ def sparse_gather_attend(q, kv: KVCache, idx, counts, weights=None, scale: Optio
 
 def sparse_decode_fused(q, kv: KVCache, sketch: Optional[SketchCache], S: float = 50.0, k_fixed: int = 0,
                         scale: Optional[float] = None, out_dtype=None, return_idx: bool = False, out=None,
-                        lse=None, idx=None, counts=None, stream=None):
-    """A6: the fused decode step -> (out, lse) or (out, lse, idx, counts)."""
+                        lse=None, idx=None, counts=None, stream=None, n_sink: int = 0, n_local: int = 0,
+                        heavy_fraction: float = 0.0):
+    """A6: the fused decode step -> (out, lse) or (out, lse, idx, counts).  With
+    n_sink / n_local / heavy_fraction: the Sink + Local + heavy budget (NEXT-1)."""
     g = geometry(q, kv, out_dtype)
-    bud = make_budget(S, k_fixed)
+    bud = make_budget(S, k_fixed, n_sink, n_local, heavy_fraction)
     scale = scale if scale is not None else 1.0 / math.sqrt(q.shape[-1])
     out = out if out is not None else torch.empty(q.shape, dtype=out_dtype or q.dtype, device=q.device)
     lse = lse if lse is not None else torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
     if return_idx and idx is None:
-        k_max = budget_k(S, kv.max_seq_len, k_fixed)
+        k_max = max(1, budget_k(S, kv.max_seq_len, k_fixed, n_sink, n_local, heavy_fraction))
         idx = torch.full((g.batch, g.num_q_heads, k_max), -1, dtype=torch.int32, device=q.device)
         counts = torch.zeros((g.batch, g.num_q_heads), dtype=torch.int32, device=q.device)
     kvs = kv.c_struct()

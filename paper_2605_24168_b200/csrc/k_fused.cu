@@ -192,8 +192,8 @@ __device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, 
 template <int G>
 __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
-    int k_fixed, uint32_t* __restrict__ thr, int* __restrict__ counters) {
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    BudgetDev bud, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* hist1 = reinterpret_cast<uint32_t*>(smem);  // [G][kHistWords] padded 2048-bin
@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     tt[u] = (i < n_slots && t < N) ? t : -1;
     if (tt[u] >= 0) raw[u] = ldg_nc_v4(sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
-  const int k = min(budget_k_dev(N, S, k_fixed), N);
+  const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
+  const int k = min(rbud.k, N);
   uint32_t key[kSampleSlots][G];
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
@@ -244,6 +245,10 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
         const int t = tt[u];
         const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
         for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(rp + c0), qc + c0, C, acc);
+      }
+      if (tt[u] < rbud.lo || tt[u] >= rbud.hi) {
+#pragma unroll
+        for (int j = 0; j < G; ++j) acc[j] = INFINITY;
       }
     }
 #pragma unroll
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
-    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch) {
+    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud) {
   constexpr int NW = kScanNT / 32;
   static_assert(NW == kScanWarps, "one band region per scan warp");
   constexpr int CW = band_region_cap(G);
@@ -448,6 +453,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
       for (int c = 0; c < 8; ++c) qr[j][c] = qc[j * 8 + c];
   }
   pdl_wait();  // the bracket comes from the sample kernel
+  const RowBudget rb = row_budget(N, bud);
   float flo[G], fsure[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -475,6 +481,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     slot_out = slot_out + 1 == kScanStages ? 0 : slot_out + 1;
     const int lim = min(stage_tok, ntok - s * stage_tok);  // valid tokens of this stage
     const int tbase = t0 + s * stage_tok;                  // first token of the stage
+    const bool edge_stage = tbase < rb.lo || tbase + lim > rb.hi;  // touches the sink / local regions
     // this warp owns bitmap words w + 8 q of the stage (the tokens it scores)
     if (lane < G * nown) s_words[own_j * kScanMaxWords + own_w] = 0u;
     // ---- phase 1: score every token; keep the candidates (key >= lo for some head)
@@ -501,6 +508,13 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
       } else if (i < stage_tok) {
         const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
         for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(src[c0 >> 3], qc + c0, C, acc);
+      }
+      if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
+        const int t = tbase + i;
+        if (t < rb.lo || t >= rb.hi) {
+#pragma unroll
+          for (int j = 0; j < G; ++j) acc[j] = INFINITY;
+        }
       }
       bool cand = false;
 #pragma unroll
@@ -561,8 +575,8 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 template <int G>
 __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv, float S,
-    int k_fixed, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    BudgetDev bud, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
     const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm, int ldw,
     float* __restrict__ scratch, int ld, int* __restrict__ counts_out, int force_fallback, int* __restrict__ err,
     int sel_cap) {
@@ -596,9 +610,10 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     s_n = 0;
   }
   pdl_wait();
-  const int k = N >= 1 ? budget_k_dev(N, S, k_fixed) : 0;
+  const RowBudget rb = row_budget(max(N, 0), bud);
+  const int k = N >= 1 ? rb.k : 0;
   uint32_t* fr = fbm + (size_t)row * ldw;
-  if (N < 1 || k > N || k < 1) {
+  if (N < 1 || k > N || (k < 1 && !budget_regions(bud))) {
     if (tid == 0) {
       set_error(err, SD_DEVERR_SEQLEN);
       if (counts_out) counts_out[row] = 0;
@@ -770,7 +785,7 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
       const uint16_t* rowp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
       float acc = 0.f;
       for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rowp + c0), qc + c0, C, &acc);
-      sr[t] = acc;
+      sr[t] = (t < rb.lo || t >= rb.hi) ? INFINITY : acc;
     }
     __syncthreads();
     auto key_at = [sr](int i) { return score_key(sr[i]); };
@@ -839,7 +854,9 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 // the low end, 1 at the high end).
 int band_capacity(int max_seq_len, Budget bud) {
   const double N = std::max(1, max_seq_len);
-  const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N) : std::ceil(N / bud.S);
+  const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N)
+                   : bud.regions() ? std::max(1.0, bud.heavy_fraction * N + bud.n_sink + bud.n_local)
+                                   : std::ceil(N / bud.S);
   const double f = std::min(1.0, (double)(kSampleThreads * kSampleSlots) / N);
   const double sig = std::sqrt(k * f * (1.0 - f));
   const double band = (2.0 * kBracketZ * sig + 2.0) / f;
@@ -859,7 +876,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     auto kern = sbs_sample_kernel<G>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
-                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, w.thr, w.counters);
+                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[0], st);
   }
@@ -873,7 +890,8 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     set_smem(kern, smem);
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
-                   geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch);
+                   geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch,
+                   bud.dev());
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
@@ -883,7 +901,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     auto kern = sbs_select_kernel<G>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(geo.B * geo.Hq), dim3(kSelNT), smem, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
-                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.S, bud.k_fixed, (const uint32_t*)w.thr,
+                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), (const uint32_t*)w.thr,
                    (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld, w.counts_out,
                    w.force_fallback, w.err, sel_cap);
     if (e != cudaSuccess) return e;

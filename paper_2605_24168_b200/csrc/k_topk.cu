@@ -22,23 +22,32 @@ constexpr int kTkThreads = 1024;
 // [count, k_max) of idx/out_scores are padded with -1 / -inf when pad != 0.
 __global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
     const float* __restrict__ scores, int ld, const int* __restrict__ seq_lens,
-    const int* __restrict__ k_from, int Hq, float S, int k_fixed, int* __restrict__ idx,
+    const int* __restrict__ k_from, int Hq, BudgetDev bud, int* __restrict__ idx,
     int* __restrict__ counts, float* __restrict__ out_scores, int k_max, int pad,
     int* __restrict__ err) {
   __shared__ SelectSmem<kTkThreads> sm;
   const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
   const int N = __ldg(seq_lens + b);
-  const int NK = k_from ? __ldg(k_from + b) : N;
-  int k = (NK >= 1 && S >= 1.f) ? budget_k_dev(NK, S, k_fixed) : 0;
-  if (k_from) k = min(k, N);
+  const bool regions = !k_from && budget_regions(bud);
+  int k, lo = 0, hi = N;
+  if (regions) {  // NEXT-1: sinks [0, lo) and locals [hi, N) rank above every score
+    const RowBudget rb = row_budget(N, bud);
+    k = rb.k;
+    lo = rb.lo;
+    hi = rb.hi;
+  } else {
+    const int NK = k_from ? __ldg(k_from + b) : N;
+    k = (NK >= 1 && bud.S >= 1.f) ? budget_k_dev(NK, bud.S, bud.k_fixed) : 0;
+    if (k_from) k = min(k, N);
+  }
   int* out = idx + (size_t)row * k_max;
   float* osc = out_scores ? out_scores + (size_t)row * k_max : nullptr;
-  if (N < 0 || k > k_max || k > N || (k < 1 && !k_from) || (!k_from && k_fixed > N)) {
+  if (N < 0 || k > k_max || k > N || (k < 1 && !k_from && !regions) || (!k_from && !regions && bud.k_fixed > N)) {
     if (tid == 0) { set_error(err, SD_DEVERR_SEQLEN); counts[row] = 0; }
     return;
   }
   const float* s = scores + (size_t)row * ld;
-  auto key_at = [s](int i) { return score_key(__ldg(s + i)); };
+  auto key_at = [s, lo, hi](int i) { return (i < lo || i >= hi) ? 0xFFFFFFFFu : score_key(__ldg(s + i)); };
   uint32_t emitted = 0;
   if (k > 0) {
     uint32_t tau, need_eq;
@@ -107,16 +116,16 @@ __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
 
 cudaError_t launch_topk(const Geo& g, const float* scores, int ld, const int* seq_lens,
                         Budget bud, int* idx, int* counts, int k_max, int* err, cudaStream_t st) {
-  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, nullptr, g.Hq, bud.S,
-                                                       bud.k_fixed, idx, counts, nullptr, k_max, 0, err);
+  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, nullptr, g.Hq, bud.dev(),
+                                                       idx, counts, nullptr, k_max, 0, err);
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const int* seq_lens,
                               const int* global_lens, Budget bud, int* idx, int* counts,
                               float* cand_scores, int k_max, int* err, cudaStream_t st) {
-  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, global_lens, g.Hq, bud.S,
-                                                       bud.k_fixed, idx, counts, cand_scores, k_max, 1,
+  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, global_lens, g.Hq, bud.dev(),
+                                                       idx, counts, cand_scores, k_max, 1,
                                                        err);
   return cudaGetLastError();
 }

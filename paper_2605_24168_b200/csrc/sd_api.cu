@@ -66,7 +66,21 @@ using namespace sd;
 
 namespace {
 
+bool budget_has_regions(const sd_budget* b) {
+  return b->n_sink != 0 || b->n_local != 0 || b->heavy_fraction != 0.f;
+}
+
+// total selected rows of one sequence (host twin of row_budget, sd_common.cuh)
 bool k_from_budget(const sd_budget* b, int N, int* k) {
+  if (budget_has_regions(b)) {
+    if (N < 0) return false;
+    const int lo = std::min(b->n_sink, N), hi = std::max(lo, N - std::min(b->n_local, N));
+    const int mid = hi - lo;
+    const int kh = b->k_fixed > 0 ? std::min(b->k_fixed, mid)
+                                  : std::min(mid, (int)floor((double)b->heavy_fraction * (double)mid + 0.5));
+    *k = lo + (N - hi) + kh;
+    return true;
+  }
   if (b->k_fixed > 0) {
     if (b->k_fixed > N) return false;
     *k = b->k_fixed;
@@ -120,11 +134,25 @@ sd_status check_sketch(const sd_sketch* sk) {
 
 sd_status check_budget(const sd_budget* b, int max_seq_len, int* k_max) {
   if (!b) return SD_ERR_INVALID_ARG;
-  if (b->n_sink != 0 || b->n_local != 0 || b->heavy_fraction != 0.f) return SD_ERR_UNSUPPORTED;
   if (b->k_fixed < 0) return SD_ERR_INVALID_ARG;
+  if (budget_has_regions(b)) {  // NEXT-1 Sink + Local + heavy
+    if (b->n_sink < 0 || b->n_local < 0 || !(b->heavy_fraction >= 0.f && b->heavy_fraction <= 1.f))
+      return SD_ERR_INVALID_ARG;
+    if (!k_from_budget(b, max_seq_len, k_max)) return SD_ERR_INVALID_ARG;
+    *k_max = std::max(*k_max, 1);
+    return SD_OK;
+  }
   if (b->k_fixed == 0 && !(b->sparsity >= 1.0f)) return SD_ERR_INVALID_ARG;
   if (!k_from_budget(b, max_seq_len, k_max)) return SD_ERR_INVALID_ARG;
   return SD_OK;
+}
+
+Budget to_budget(const sd_budget* b) {
+  Budget r{b->sparsity, b->k_fixed};
+  r.n_sink = b->n_sink;
+  r.n_local = b->n_local;
+  r.heavy_fraction = b->heavy_fraction;
+  return r;
 }
 
 sd_status check_ws(const void* ws, size_t ws_bytes, size_t need) {
@@ -166,8 +194,8 @@ const char* sd_version(void) { return "sdattn 0.1 (sm_100a)"; }
 
 sd_status sd_budget_k(const sd_budget* budget, int32_t N, int32_t* k) {
   if (!budget || !k || N < 1) return SD_ERR_INVALID_ARG;
-  if (budget->k_fixed < 0) return SD_ERR_INVALID_ARG;
-  if (budget->k_fixed == 0 && !(budget->sparsity >= 1.0f)) return SD_ERR_INVALID_ARG;
+  int unused;
+  SD_TRY(check_budget(budget, N, &unused));
   int kk;
   if (!k_from_budget(budget, N, &kk)) return SD_ERR_INVALID_ARG;
   *k = kk;
@@ -234,7 +262,7 @@ sd_status sd_topk_select(const sd_geometry* geom, const float* scores, int32_t l
   SD_TRY(check_budget(budget, max_seq_len, &kb));
   if (!scores || !seq_lens || !idx || !counts || ld < max_seq_len || k_max < kb) return SD_ERR_INVALID_ARG;
   SD_TRY(check_ws(ws, ws_bytes, 256));
-  Budget bud{budget->sparsity, budget->k_fixed};
+  const Budget bud = to_budget(budget);
   return cuda_status(launch_topk(g, scores, ld, seq_lens, bud, idx, counts, k_max,
                                  reinterpret_cast<int*>(ws), (cudaStream_t)stream));
 }
@@ -279,7 +307,7 @@ sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sk
   SD_TRY(check_ws(ws, ws_bytes, L.total));
   cudaStream_t st = (cudaStream_t)stream;
   int* err = reinterpret_cast<int*>(ws);
-  Budget bud{budget->sparsity, budget->k_fixed};
+  const Budget bud = to_budget(budget);
   const int rows = g.B * g.Hq;
   float* part = reinterpret_cast<float*>(wsp(ws, L.part));
   if (!sketch) {
@@ -406,6 +434,7 @@ sd_status sd_seqshard_local_topk(const sd_geometry* geom, const sd_paged_kv* kv,
   Geo g;
   SD_TRY(check_geom(geom, kv->max_seq_len, &g));
   SD_TRY(check_sketch(sketch));
+  if (budget && budget_has_regions(budget)) return SD_ERR_UNSUPPORTED;  // sinks / locals are global positions
   int kg;
   SD_TRY(check_budget(budget, max_global_seq_len, &kg));
   if (!q || !global_seq_lens || !cand_scores || !cand_idx || k_max < kg ||
@@ -417,7 +446,7 @@ sd_status sd_seqshard_local_topk(const sd_geometry* geom, const sd_paged_kv* kv,
   int* err = reinterpret_cast<int*>(ws);
   float* scores = reinterpret_cast<float*>(wsp(ws, L.scores));
   int* counts = reinterpret_cast<int*>(wsp(ws, L.counts));
-  Budget bud{budget->sparsity, budget->k_fixed};
+  const Budget bud = to_budget(budget);
   SD_CUDA(launch_index_score(g, *kv, sketch, q, scores, L.ld, st));
   return cuda_status(launch_topk_shard(g, scores, L.ld, kv->seq_lens, global_seq_lens, bud, cand_idx,
                                        counts, cand_scores, k_max, err, st));
@@ -431,7 +460,8 @@ sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv,
   SD_TRY(check_kv(kv, true));
   Geo g;
   SD_TRY(check_geom(geom, kv->max_seq_len, &g));
-  if (!budget || (budget->n_sink | budget->n_local) || budget->heavy_fraction != 0.f) return SD_ERR_INVALID_ARG;
+  if (!budget) return SD_ERR_INVALID_ARG;
+  if (budget_has_regions(budget)) return SD_ERR_UNSUPPORTED;
   if (budget->k_fixed == 0 && !(budget->sparsity >= 1.0f)) return SD_ERR_INVALID_ARG;
   if (!q || !global_seq_lens || !all_cand || !cand_idx || !part_o || !part_lse || k_max < 1 || parts < 1 ||
       rank < 0 || rank >= parts || !(scale > 0.f))
@@ -442,7 +472,7 @@ sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv,
   int* err = reinterpret_cast<int*>(ws);
   int* surv = reinterpret_cast<int*>(wsp(ws, L.idx));
   int* surv_cnt = reinterpret_cast<int*>(wsp(ws, L.counts));
-  Budget bud{budget->sparsity, budget->k_fixed};
+  const Budget bud = to_budget(budget);
   SD_CUDA(launch_seqshard_cut(g, all_cand, cand_idx, parts, rank, global_seq_lens, bud, k_max, surv,
                               surv_cnt, err, st));
   const int rows = g.B * g.Hq;

@@ -33,6 +33,42 @@ __device__ __forceinline__ int budget_k_dev(int N, float S, int k_fixed) {
   return k;
 }
 
+// NEXT-1 (Sink + Local + heavy): with n_sink, n_local or
+// heavy_fraction non-zero the row keeps the sinks [0, lo) and the locals
+// [hi, N) (lo = min(n_sink, N), hi = max(lo, N - min(n_local, N))) plus the
+// top-kh tokens of the middle [lo, hi): kh = min(k_fixed, mid) if k_fixed > 0,
+// else min(mid, floor(heavy_fraction * mid + 1/2)) (round half up).
+// Implemented everywhere as "sink / local tokens score +inf" and a total
+// k = lo + (N - hi) + kh, so the selection stays a plain top-k.
+struct BudgetDev {
+  float S;
+  int k_fixed, n_sink, n_local;
+  float heavy_fraction;
+};
+struct RowBudget {
+  int lo, hi, k;  // middle region [lo, hi), total selected k (0 allowed in NEXT-1 mode)
+};
+__device__ __forceinline__ bool budget_regions(const BudgetDev& b) {
+  return b.n_sink != 0 || b.n_local != 0 || b.heavy_fraction != 0.f;
+}
+__device__ __forceinline__ RowBudget row_budget(int N, const BudgetDev& b) {
+  RowBudget r;
+  if (!budget_regions(b)) {
+    r.lo = 0;
+    r.hi = N;
+    r.k = budget_k_dev(N, b.S, b.k_fixed);
+    return r;
+  }
+  r.lo = min(b.n_sink, N);
+  r.hi = max(r.lo, N - min(b.n_local, N));
+  const int mid = r.hi - r.lo;
+  int kh;
+  if (b.k_fixed > 0) kh = min(b.k_fixed, mid);
+  else kh = min(mid, (int)floor((double)b.heavy_fraction * (double)mid + 0.5));
+  r.k = r.lo + (N - r.hi) + kh;
+  return r;
+}
+
 // ---------------------------------------------------------------- radix keys
 // Order-preserving map fp32 -> uint32 (larger score -> larger key).  -0.0 is
 // canonicalised to +0.0 so that equal scores give equal keys (ties then go to

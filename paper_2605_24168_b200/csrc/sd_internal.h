@@ -27,6 +27,10 @@ struct Geo {
 struct Budget {
   float S;
   int k_fixed;
+  int n_sink = 0, n_local = 0;
+  float heavy_fraction = 0.f;
+  BudgetDev dev() const { return BudgetDev{S, k_fixed, n_sink, n_local, heavy_fraction}; }
+  bool regions() const { return n_sink != 0 || n_local != 0 || heavy_fraction != 0.f; }
 };
 
 // Workspace carve-up; every region is 256-byte aligned.  Computed identically

@@ -39,6 +39,27 @@ def check_selection(idx_row, count, scores, k):
     return sel
 
 
+def check_region_selection(idx_row, count, scores, n_sink, n_local, heavy_fraction=0.0, k_abs=0):
+    """NEXT-1: all sinks [0, lo) and locals [hi, N) kept, plus the
+    middle's top-kh under the same tolerance rule as check_selection."""
+    N = scores.shape[0]
+    lo = min(n_sink, N)
+    hi = max(lo, N - min(n_local, N))
+    kh = oracle.heavy_budget(N, n_sink, n_local, heavy_fraction, k_abs)
+    total = lo + (N - hi) + kh
+    assert count == total, f"count {count} != {total}"
+    sel = np.asarray(idx_row[:count], dtype=np.int64)
+    assert np.all(np.diff(sel) > 0), "indices not strictly increasing"
+    edge = np.concatenate([np.arange(0, lo), np.arange(hi, N)])
+    assert np.isin(edge, sel).all(), "a sink / local token is missing"
+    mid = sel[(sel >= lo) & (sel < hi)]
+    if kh > 0:
+        check_selection(mid - lo, kh, scores[lo:hi], kh)
+    else:
+        assert mid.size == 0
+    return sel
+
+
 def rel_err(o, ref):
     o = np.asarray(o, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)

@@ -68,6 +68,31 @@ def test_budget_rejections(lib):
     assert lib.sd_budget_k(ctypes.byref(C.Budget(2.0, 10, 0, 0, 0.0)), 10, ctypes.byref(k)) == 0 and k.value == 10
 
 
+@pytest.mark.parametrize("N,n_sink,n_local,hf,k_abs", [(20000, 128, 128, 0.20, 0), (20000, 128, 128, 0.02, 0),
+                                                       (131072, 128, 128, 0.02, 0), (200, 128, 128, 0.5, 0),
+                                                       (5000, 64, 0, 0.0, 16), (77, 0, 32, 0.0, 0),
+                                                       (1000, 0, 0, 0.125, 0)])
+def test_budget_sink_local_heavy_matches_oracle(lib, N, n_sink, n_local, hf, k_abs):
+    """NEXT-1 budget: sinks + locals + the middle's heavy
+    budget, against the oracle's heavy_budget (AC8: 4205 rows at N=20000)."""
+    from paper_2605_24168_b200 import _capi as C
+    k = C.c_i32()
+    assert lib.sd_budget_k(ctypes.byref(C.Budget(1.0, k_abs, n_sink, n_local, hf)), N, ctypes.byref(k)) == 0
+    lo = min(n_sink, N)
+    hi = max(lo, N - min(n_local, N))
+    assert k.value == lo + (N - hi) + oracle.heavy_budget(N, n_sink, n_local, hf, k_abs)
+    if (N, n_sink, n_local, hf) == (20000, 128, 128, 0.20):
+        assert k.value == 4205
+
+
+def test_budget_sink_local_rejections(lib):
+    from paper_2605_24168_b200 import _capi as C
+    k = C.c_i32()
+    for bad in (C.Budget(1.0, 0, -1, 0, 0.0), C.Budget(1.0, 0, 0, -4, 0.0), C.Budget(1.0, 0, 4, 4, 1.5),
+                C.Budget(1.0, 0, 4, 4, float("nan"))):
+        assert lib.sd_budget_k(ctypes.byref(bad), 100, ctypes.byref(k)) == C.SD_ERR_INVALID_ARG
+
+
 def _geom(C, **kw):
     g = dict(batch=2, num_q_heads=32, num_kv_heads=8, head_dim=128, page_size=16, max_pages_per_seq=64,
              kv_dtype=C.SD_BF16, q_dtype=C.SD_BF16, out_dtype=C.SD_BF16)

@@ -12,7 +12,8 @@ import torch
 
 import oracle
 import workloads
-from parity import (OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_selection, host_subcase, rel_err)
+from parity import (OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_region_selection, check_selection, host_subcase,
+                    rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -261,6 +262,54 @@ def test_fused_timed_matches_untimed(cuda_lib):
     o2, l2, ph = sd.api.sparse_decode_fused_timed(case.q, kv, sk, S=50.0, scale=SCALE)
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
     assert set(ph) == set(sd.api.FUSED_PHASES) and all(v >= 0 for v in ph.values()), ph
+
+
+NEXT1_CASES = [(128, 128, 0.20, 0), (128, 128, 0.02, 0), (64, 0, 0.0, 16), (0, 32, 0.05, 0), (300, 300, 0.1, 0)]
+
+
+@pytest.mark.parametrize("n_sink,n_local,hf,k_abs", NEXT1_CASES)
+@pytest.mark.parametrize("mode", ["sketch", "exact"])
+def test_fused_sink_local_heavy(cuda_lib, n_sink, n_local, hf, k_abs, mode):
+    """NEXT-1 Sink + Local + heavy fraction through the
+    fused entry (sample/scan/select in sketch mode, radix top-k in exact mode)."""
+    sd = cuda_lib
+    lens = [20000, 5000, 200]
+    case = workloads.make_case(len(lens), 8, 2, lens, seed=71, dist="needle", n_needles=24, sketch=mode == "sketch")
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, sk = _kv(sd, dc)
+    out, lse, idx, cnt = sd.sparse_decode_fused(dc.q, kv, sk if mode == "sketch" else None, S=1.0, k_fixed=k_abs,
+                                                scale=SCALE, out_dtype=torch.float32, return_idx=True,
+                                                n_sink=n_sink, n_local=n_local, heavy_fraction=hf)
+    assert sd.read_device_error() == 0
+    out, lse, idx, cnt = out.cpu().numpy(), lse.cpu().numpy(), idx.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(case.B):
+        for h in range(case.Hq):
+            scores = oracle.index_scores(inp, b, h, mode)
+            sel = check_region_selection(idx[b, h], cnt[b, h], scores, n_sink, n_local, hf, k_abs)
+            ro, rl = oracle.attend_given(inp, b, h, sel, SCALE)
+            assert rel_err(out[b, h], ro) <= 1e-4, (b, h)
+            check_lse(lse[b, h], rl)
+
+
+@pytest.mark.parametrize("n_sink,n_local,hf,k_abs", NEXT1_CASES)
+def test_topk_sink_local_heavy_bit_exact(cuda_lib, n_sink, n_local, hf, k_abs):
+    """sd_topk_select with a NEXT-1 budget equals oracle.sink_local_heavy_select
+    exactly on fp32 scores with heavy ties."""
+    sd = cuda_lib
+    g = torch.Generator().manual_seed(5)
+    B, Hq, N = 2, 4, 7000
+    sc = torch.randint(-40, 40, (B, Hq, N), generator=g).float() / 8.0  # many exact ties
+    lens = torch.tensor([N, 1500], dtype=torch.int32)
+    idx, cnt = sd.topk_select(sc.cuda(), lens.cuda(), N, S=1.0, k_fixed=k_abs, n_sink=n_sink, n_local=n_local,
+                              heavy_fraction=hf)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(B):
+        n = int(lens[b])
+        for h in range(Hq):
+            ref = oracle.sink_local_heavy_select(sc[b, h, :n].double().numpy(), n_sink, n_local, hf, k_abs)
+            assert cnt[b, h] == ref.size
+            np.testing.assert_array_equal(idx[b, h, :cnt[b, h]], ref)
 
 
 @pytest.mark.parametrize("S", [1.0, 2.0, 10.0, 100.0, 500.0])
