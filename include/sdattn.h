@@ -189,6 +189,25 @@ sd_status sd_topk_select(const sd_geometry* geom, const float* scores, int32_t l
                          const sd_budget* budget, int32_t* idx, int32_t* counts,
                          int32_t k_max, void* ws, size_t ws_bytes, sd_stream stream);
 
+/* ---- NEXT-2: weighted stochastic selection (vAttention stand-in; P:145,
+ * P:158 name the method, S:233-241 fix this design) ---------------------------
+ * For every (b, h) with N_b tokens, scores fp32 [B][Hq][ld] and u fp32
+ * [B][Hq][ld] (one uniform key in [0, 1) per token: the random draw is an
+ * input, so that the CPU oracle sees the same draw):
+ *   det    = top-k_d by score, k_d = min(k_det, N_b), ties to the lower index, weight 1;
+ *   sample = the ns = min(n_samples, N_b - k_d) other tokens with the smallest
+ *            u (ties to the lower index), weight (N_b - k_d) / ns (1 when ns
+ *            covers the whole remainder);
+ * idx[b][h][0..counts) = det U sample in increasing index order, weights the
+ * matching weights (feed both to sd_sparse_gather_attend).  k_max >=
+ * min(k_det + n_samples, max_seq_len); ws from sd_workspace_size_k(geom,
+ * max_seq_len, k_max). */
+sd_status sd_stochastic_select(const sd_geometry* geom, const float* scores, int32_t ld,
+                               const float* u, const int32_t* seq_lens, int32_t max_seq_len,
+                               int32_t k_det, int32_t n_samples, int32_t* idx, float* weights,
+                               int32_t* counts, int32_t k_max, void* ws, size_t ws_bytes,
+                               sd_stream stream);
+
 /* ---- A4+A5: gather-attend with split-k LSE merge ("weighted attention
  * given sparse index and associated weights") ---------------------
  * For every (b, h) with I = idx[b][h][0..counts[b][h]) and weights w (NULL = 1):

@@ -64,6 +64,8 @@ _PROTOS = {
     "sd_sparse_index_score": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, c_vp, c_i32, c_vp]),
     "sd_topk_select": (c_i32, [P(Geometry), c_vp, c_i32, c_vp, c_i32, P(Budget), c_vp, c_vp, c_i32, c_vp,
                                c_size, c_vp]),
+    "sd_stochastic_select": (c_i32, [P(Geometry), c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                     c_i32, c_vp, c_size, c_vp]),
     "sd_sparse_gather_attend": (c_i32, [P(Geometry), P(PagedKV), c_vp, c_vp, c_vp, c_i32, c_vp, c_f32, c_vp,
                                         c_vp, c_vp, c_size, c_vp]),
     "sd_sparse_decode_fused": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_f32, c_vp, c_vp,

@@ -206,6 +206,27 @@ def topk_select(scores, seq_lens, max_seq_len: int, S: float = 1.0, k_fixed: int
     return idx, counts
 
 
+def stochastic_select(scores, u, seq_lens, max_seq_len: int, k_det: int, n_samples: int, num_kv_heads=None,
+                      k_max: Optional[int] = None, stream=None):
+    """NEXT-2: (idx int32 [B][Hq][k_max] ascending, weights fp32 [B][Hq][k_max],
+    counts int32 [B][Hq]) = deterministic top-k_det + n_samples smallest-u
+    remainder tokens weighted |R| / n_samples (u: the uniform draw, an input)."""
+    B, Hq, ld = scores.shape
+    if k_max is None:
+        k_max = max(1, min(k_det + n_samples, max_seq_len))
+    Hkv = num_kv_heads or Hq
+    g = C.Geometry(B, Hq, Hkv, 128, 16, (max_seq_len + 15) // 16, C.SD_BF16, C.SD_BF16, C.SD_BF16)
+    idx = torch.full((B, Hq, k_max), -1, dtype=torch.int32, device=scores.device)
+    wts = torch.zeros((B, Hq, k_max), dtype=torch.float32, device=scores.device)
+    counts = torch.zeros((B, Hq), dtype=torch.int32, device=scores.device)
+    ws = workspace(_ws_bytes_budget(g, None, max_seq_len, k_max), scores.device, stream)
+    p, n = _ws_ptr(ws)
+    _check(C.load().sd_stochastic_select(ctypes.byref(g), _ptr(scores), ld, _ptr(u), _ptr(seq_lens),
+                                         int(max_seq_len), int(k_det), int(n_samples), _ptr(idx), _ptr(wts),
+                                         _ptr(counts), int(k_max), p, n, _stream(stream)), "sd_stochastic_select")
+    return idx, wts, counts
+
+
 def sparse_gather_attend(q, kv: KVCache, idx, counts, weights=None, scale: Optional[float] = None,
                          out_dtype=None, out=None, lse=None, stream=None):
     """A4+A5: weighted attention over per-head index lists -> (out [B][Hq][D], lse [B][Hq])."""

@@ -267,6 +267,22 @@ sd_status sd_topk_select(const sd_geometry* geom, const float* scores, int32_t l
                                  reinterpret_cast<int*>(ws), (cudaStream_t)stream));
 }
 
+sd_status sd_stochastic_select(const sd_geometry* geom, const float* scores, int32_t ld, const float* u,
+                               const int32_t* seq_lens, int32_t max_seq_len, int32_t k_det, int32_t n_samples,
+                               int32_t* idx, float* weights, int32_t* counts, int32_t k_max, void* ws,
+                               size_t ws_bytes, sd_stream stream) {
+  Geo g;
+  SD_TRY(check_geom(geom, max_seq_len, &g));
+  if (!scores || !u || !seq_lens || !idx || !weights || !counts || ld < max_seq_len || k_det < 0 || n_samples < 0)
+    return SD_ERR_INVALID_ARG;
+  if (k_max < 1 || k_max < std::min((long long)k_det + n_samples, (long long)max_seq_len)) return SD_ERR_INVALID_ARG;
+  const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, max_seq_len, true, k_max);
+  SD_TRY(check_ws(ws, ws_bytes, L.total));
+  return cuda_status(launch_stochastic_select(g, scores, u, ld, seq_lens, k_det, n_samples,
+                                              reinterpret_cast<uint32_t*>(wsp(ws, L.fbm)), L.ldw, idx, weights,
+                                              counts, k_max, reinterpret_cast<int*>(ws), (cudaStream_t)stream));
+}
+
 sd_status sd_sparse_gather_attend(const sd_geometry* geom, const sd_paged_kv* kv, const void* q,
                                   const int32_t* idx, const int32_t* counts, int32_t k_max,
                                   const float* weights, float scale, void* out, float* lse, void* ws,

@@ -95,6 +95,11 @@ cudaError_t launch_lse_merge(int parts, int rows, const float* part_o, const flo
 
 int choose_splits(int rows, int work_per_row, int min_per_split);
 
+// NEXT-2 weighted stochastic selection (k_stoch.cu); mark: [B*Hq][ldw] scratch
+cudaError_t launch_stochastic_select(const Geo& g, const float* scores, const float* u, int ld, const int* seq_lens,
+                                     int k_det, int n_samples, uint32_t* mark, int ldw, int* idx, float* weights,
+                                     int* counts, int k_max, int* err, cudaStream_t st);
+
 // ---- fused sample-bracket select (k_fused.cu) -------------------------------
 struct SbsBuffers {
   uint32_t* thr;

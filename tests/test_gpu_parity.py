@@ -312,6 +312,53 @@ def test_topk_sink_local_heavy_bit_exact(cuda_lib, n_sink, n_local, hf, k_abs):
             np.testing.assert_array_equal(idx[b, h, :cnt[b, h]], ref)
 
 
+@pytest.mark.parametrize("k_det,n_samples", [(16, 64), (10, 0), (1, 40), (10, 100000), (300, 700)])
+def test_stochastic_select_matches_oracle(cuda_lib, k_det, n_samples):
+    """NEXT-2: the GPU selection and weights equal
+    oracle.stochastic_select on the same scores and the same uniform draw
+    (ties in scores and in u to the lower index)."""
+    sd = cuda_lib
+    g = torch.Generator().manual_seed(9)
+    B, Hq, N = 2, 4, 5000
+    sc = torch.randint(-30, 30, (B, Hq, N), generator=g).float() / 4.0
+    u = torch.randint(0, 4000, (B, Hq, N), generator=g).float() / 4096.0  # uniform keys with ties
+    lens = torch.tensor([N, 777], dtype=torch.int32)
+    idx, wts, cnt = sd.api.stochastic_select(sc.cuda(), u.cuda(), lens.cuda(), N, k_det, n_samples)
+    idx, wts, cnt = idx.cpu().numpy(), wts.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(B):
+        n = int(lens[b])
+        for h in range(Hq):
+            ri, rw = oracle.stochastic_select(sc[b, h, :n].double().numpy(), min(k_det, n), n_samples,
+                                              u[b, h, :n].double().numpy())
+            assert cnt[b, h] == ri.size, (b, h, cnt[b, h], ri.size)
+            np.testing.assert_array_equal(idx[b, h, :ri.size], ri)
+            np.testing.assert_allclose(wts[b, h, :ri.size], rw, rtol=1e-6)
+
+
+def test_stochastic_weighted_attend_end_to_end(cuda_lib):
+    """NEXT-2 selection on the GPU's own index scores -> weighted gather-attend
+    == oracle.attend_given(selection, weights)."""
+    sd = cuda_lib
+    case = workloads.make_case(2, 8, 2, [6000, 900], seed=77)
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, sk = _kv(sd, dc)
+    N = int(case.seq_lens.max())
+    scores = sd.sparse_index_score(dc.q, kv, sk)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    u = torch.rand(scores.shape, generator=gen, device="cuda")
+    idx, wts, cnt = sd.api.stochastic_select(scores, u, dc.seq_lens, N, 32, 96, num_kv_heads=2)
+    out, lse = sd.sparse_gather_attend(dc.q, kv, idx, cnt, weights=wts, scale=SCALE, out_dtype=torch.float32)
+    out, lse = out.cpu().numpy(), lse.cpu().numpy()
+    idx, wts, cnt = idx.cpu().numpy(), wts.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(case.B):
+        for h in range(case.Hq):
+            c = int(cnt[b, h])
+            ro, rl = oracle.attend_given(inp, b, h, idx[b, h, :c], SCALE, weights=wts[b, h, :c].astype(np.float64))
+            assert rel_err(out[b, h], ro) <= 1e-4
+            check_lse(lse[b, h], rl)
+
+
 @pytest.mark.parametrize("S", [1.0, 2.0, 10.0, 100.0, 500.0])
 def test_fused_exact_mode_sparsity_sweep(cuda_lib, S):
     lens = [3, 257, 6000]
