@@ -128,7 +128,8 @@ def workload_name(cfg_name, cfg, world):
             f"page 16, {'bf16' if cfg['dtype'].is_floating_point and cfg['dtype'].itemsize == 2 else 'fp32'} KV, "
             + ("sketch C=8 bf16" if cfg["sketch"] else "exact scores"))
     if world > 1:
-        base += f"; KV-head sharded over {world} GPUs (per-rank shard shown)"
+        base += (f"; KV-head sharded over {world} GPUs: each rank serves all {cfg['B']} sequences with "
+                 f"{cfg['Hkv']} of the {cfg['Hkv'] * world} KV heads (per-rank shard shown)")
     return base
 
 
@@ -228,10 +229,18 @@ def main():
     world, rank, local = dist_env()
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    # BENCH_SHARE_DEVICE=1 + BENCH_DIST_BACKEND=gloo: every rank on cuda:0 (a
+    # smoke test of the multi-rank path on one GPU; not a scaling measurement)
+    if os.environ.get("BENCH_SHARE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     sd.load_library()
 
     case, cfg = rank_case(args.config, world, rank, dev)
@@ -282,11 +291,13 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * B * 1000.0 / ms_step
+    # KV-head sharding: every rank serves all B sequences (its 1/N of the heads),
+    # so the job decodes B tokens per step (B = 16 N: weak scaling)
+    value = B * 1000.0 / ms_step
 
     # end to end through the public API with pinned host buffers
     q_host = torch.stack([q.cpu() for q in qs]).pin_memory()
@@ -308,10 +319,10 @@ def main():
     torch.cuda.synchronize()
     ms_e2e = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms_e2e], device=dev)
+        t = torch.tensor([ms_e2e], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    e2e_value = world * B * 1000.0 / (ms_e2e / args.steps)
+    e2e_value = B * 1000.0 / (ms_e2e / args.steps)
 
     # dense decode on the same cache (speedup context)
     dense = None
@@ -361,7 +372,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16" if case.dtype == torch.bfloat16 else "f32", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, cfg, world), "global_batch": B * world,
+        "config": {"workload": workload_name(args.config, cfg, world), "global_batch": B,
                    "seq_len": cfg["N"], "sparsity": S, "k": k,
                    "l2": "inputs > L2: 936 MB touched per step at cfg3, 4 rotating query sets",
                    "parallelism": f"kv-head-shard{world}" if world > 1 else "single-gpu"},
