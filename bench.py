@@ -126,7 +126,8 @@ def rank_case(cfg_name, world, rank, device):
 def workload_name(cfg_name, cfg, world):
     base = (f"{cfg_name}: B={cfg['B']}, N={cfg['N']}, S={cfg['S']:g}, Hq={cfg['Hq']}, Hkv={cfg['Hkv']}, D=128, "
             f"page 16, {'bf16' if cfg['dtype'].is_floating_point and cfg['dtype'].itemsize == 2 else 'fp32'} KV, "
-            + ("sketch C=8 bf16" if cfg["sketch"] else "exact scores"))
+            + ((f"sketch C=8 {'fp8 e4m3' if 'float8' in str(cfg.get('sketch_dtype', '')) else 'bf16'}")
+               if cfg["sketch"] else "exact scores"))
     if world > 1:
         base += (f"; KV-head sharded over {world} GPUs: each rank serves all {cfg['B']} sequences with "
                  f"{cfg['Hkv']} of the {cfg['Hkv'] * world} KV heads (per-rank shard shown)")
@@ -263,6 +264,7 @@ def main():
     E = union_rows(idx, cnt, Hkv)
     k = sd.budget_k(S, cfg["N"])
     model = RL.sparse_step_bytes(B, Hq, Hkv, cfg["N"], k, w=case.dtype.itemsize, exact=not cfg["sketch"],
+                                 sketch_w=case.sketch_pages.element_size() if case.sketch_pages is not None else 2,
                                  union_rows_total=E)
     del idx, cnt
     sd.clear_device_error()

@@ -64,7 +64,7 @@ enum {
 };
 
 typedef int32_t sd_dtype;
-enum { SD_BF16 = 0, SD_F32 = 1 };
+enum { SD_BF16 = 0, SD_F32 = 1, SD_E4M3 = 2 /* fp8 e4m3: sketch pages only */ };
 
 typedef void* sd_stream; /* cudaStream_t */
 
@@ -111,6 +111,9 @@ typedef struct {
   const void* pages;
   const int32_t* channel_ids;
   int32_t channels;
+  sd_dtype dtype;  /* SD_BF16 (0, default) or SD_E4M3 (NEXT-4 low-precision sketch,
+                      P:301; channels == 8 only); the scores are the same fp32
+                      fma chain over the exactly-converted channel values */
 } sd_sketch;
 
 /* Sparsity budget ("each query-head attends to 1/S fraction of total

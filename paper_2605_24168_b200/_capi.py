@@ -21,6 +21,7 @@ SD_ERR_DEVICE_CHECK = 5
 
 SD_BF16 = 0
 SD_F32 = 1
+SD_E4M3 = 2  # fp8 e4m3 (sketch pages only, NEXT-4)
 
 DEVERR = {0: "none", 1: "index out of range", 2: "indices not strictly increasing", 3: "empty index list",
           4: "weight <= 0 or non-finite", 5: "bad sequence length / budget", 6: "candidate overflow"}
@@ -43,7 +44,7 @@ class PagedKV(ctypes.Structure):
 
 
 class Sketch(ctypes.Structure):
-    _fields_ = [("pages", c_vp), ("channel_ids", c_vp), ("channels", c_i32)]
+    _fields_ = [("pages", c_vp), ("channel_ids", c_vp), ("channels", c_i32), ("dtype", c_i32)]
 
 
 class Budget(ctypes.Structure):

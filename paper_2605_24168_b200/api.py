@@ -75,7 +75,8 @@ class KVCache:
 
 @dataclass
 class SketchCache:
-    """Double-Sparsity sketch: pages bf16 [P][Hkv][page_size][C], channel_ids int32 [B][Hkv][C]."""
+    """Double-Sparsity sketch: pages bf16 or fp8 e4m3 (NEXT-4) [P][Hkv][page_size][C],
+    channel_ids int32 [B][Hkv][C]."""
     pages: torch.Tensor
     channel_ids: torch.Tensor
 
@@ -86,7 +87,8 @@ class SketchCache:
         return cls(case.sketch_pages, case.channel_ids)
 
     def c_struct(self) -> C.Sketch:
-        return C.Sketch(_ptr(self.pages), _ptr(self.channel_ids), int(self.pages.shape[-1]))
+        dt = C.SD_E4M3 if self.pages.dtype == torch.float8_e4m3fn else C.SD_BF16
+        return C.Sketch(_ptr(self.pages), _ptr(self.channel_ids), int(self.pages.shape[-1]), dt)
 
 
 def geometry(q: torch.Tensor, kv: KVCache, out_dtype: Optional[torch.dtype] = None) -> C.Geometry:

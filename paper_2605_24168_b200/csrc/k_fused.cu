@@ -189,9 +189,9 @@ __device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, 
   *res_out = __shfl_sync(0xffffffffu, res, src);
 }
 
-template <int G>
+template <int G, class Sk>
 __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
-    const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
+    const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     BudgetDev bud, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = kSampleThreads * kSampleSlots;
@@ -222,14 +222,14 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   const int ns_pages = (npg + spg - 1) / spg;
   const int n_slots = ns_pages * 16;
   // all loads of this thread first (latency-bound gather of sample pages)
-  uint4 raw[kSampleSlots];
+  typename Sk::Raw raw[kSampleSlots];
   int tt[kSampleSlots];
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
     const int i = tid + u * kSampleThreads;
     const int t = (i >> 4) * spg * 16 + (i & 15);
     tt[u] = (i < n_slots && t < N) ? t : -1;
-    if (tt[u] >= 0) raw[u] = ldg_nc_v4(sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
+    if (tt[u] >= 0) raw[u] = Sk::load8(sk, sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
   const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
   const int k = min(rbud.k, N);
@@ -240,11 +240,11 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
 #pragma unroll
     for (int j = 0; j < G; ++j) acc[j] = 0.f;
     if (tt[u] >= 0) {
-      sketch_fma8<G>(raw[u], qc, C, acc);
+      sketch_fma8<G, Sk>(raw[u], qc, C, acc);
       if (C > 8) {
         const int t = tt[u];
-        const uint16_t* rp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(rp + c0), qc + c0, C, acc);
+        const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G, Sk>(Sk::load8(sk, re + c0), qc + c0, C, acc);
       }
       if (tt[u] < rbud.lo || tt[u] >= rbud.hi) {
 #pragma unroll
@@ -362,7 +362,7 @@ __device__ __forceinline__ void load_scores(float (&sc)[G], const float* src) {
   }
 }
 
-template <int G, bool C8>
+template <int G, bool C8, class Sk>
 __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
@@ -373,7 +373,9 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   constexpr int CW = band_region_cap(G);
   extern __shared__ __align__(128) unsigned char smem[];
   const int stage_tok = (kScanStageTok8 * 8 / C) & ~31;  // whole bitmap words per stage
-  const int stage_bytes = kScanStageTok8 * 16;
+  const int stage_bytes = kScanStageTok8 * 16;  // ring slot size (bf16 rows; fp8 rows use half)
+  constexpr int kRowB = 8 * Sk::kBytes;           // C8: one token's sketch row (16 B bf16, 8 B fp8)
+  constexpr int kTpc = 16 / kRowB;                // C8: tokens per 16-B copy
   unsigned char* ring = smem;
   float* qc = reinterpret_cast<float*>(ring + (size_t)kScanStages * stage_bytes);  // [G][C]
   int* s_pages = reinterpret_cast<int*>(qc + G * C);                                // [kRangeTok / 16]
@@ -404,27 +406,27 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int cpt = C >> 3;  // 16-B chunks per token
   // C8: thread tid copies tokens tid + 256 u of a stage: page (tid >> 4) + 16 u
   // of the stage's 64, slot tid & 15 (fixed per thread)
-  const char* tb = skb + ((size_t)g * kPS + (tid & 15)) * 16;
-  const uint32_t page_bytes = (uint32_t)Hkv * kPS * 16;
+  const char* tb = skb + ((size_t)g * kPS + ((tid * kTpc) & 15)) * kRowB;
+  const uint32_t page_bytes = (uint32_t)Hkv * kPS * kRowB;
   int slot_in = 0;  // ring slot of the next issue
   auto issue = [&](int s) {
     if (s < nst) {
       unsigned char* st = ring + (size_t)slot_in * stage_bytes;
       if (C8) {
-        const int* sp = s_pages + (s * kScanStageTok8 >> 4) + (tid >> 4);
+        const int* sp = s_pages + (s * kScanStageTok8 >> 4) + ((tid * kTpc) >> 4);
         if ((s + 1) * kScanStageTok8 <= ntok) {  // full stage: plain copies
 #pragma unroll
-          for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
+          for (int u = 0; u < kScanStageTok8 / kScanNT / kTpc; ++u) {
             const uint32_t d = smem_u32(st + (size_t)(tid + u * kScanNT) * 16);
-            const char* src = tb + (size_t)(uint32_t)sp[u * (kScanNT >> 4)] * page_bytes;
+            const char* src = tb + (size_t)(uint32_t)sp[u * (kScanNT * kTpc >> 4)] * page_bytes;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
           }
         } else {  // the range's tail: rows past the end are zero-filled
 #pragma unroll
-          for (int u = 0; u < kScanStageTok8 / kScanNT; ++u) {
-            const int ti = tid + u * kScanNT;
-            const bool valid = s * kScanStageTok8 + ti < ntok;
-            const char* src = valid ? tb + (size_t)(uint32_t)sp[u * (kScanNT >> 4)] * page_bytes : skb;
+          for (int u = 0; u < kScanStageTok8 / kScanNT / kTpc; ++u) {
+            const int ti = tid + u * kScanNT;  // 16-B chunk: tokens kTpc ti ..
+            const bool valid = s * kScanStageTok8 + ti * kTpc < ntok;
+            const char* src = valid ? tb + (size_t)(uint32_t)sp[u * (kScanNT * kTpc >> 4)] * page_bytes : skb;
             cp_async16_zf(st + (size_t)ti * 16, src, valid);
           }
         }
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
       for (int j = 0; j < G; ++j) acc[j] = 0.f;
       if (C8) {
         float x[8];
-        unpack_bf16x8(*reinterpret_cast<const uint4*>(st + (size_t)(i < stage_tok ? i : 0) * 16), x);
+        Sk::unpack(*reinterpret_cast<const typename Sk::Raw*>(st + (size_t)(i < stage_tok ? i : 0) * kRowB), x);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           if (G == 1) {
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         }
       } else if (i < stage_tok) {
         const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
-        for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(src[c0 >> 3], qc + c0, C, acc);
+        for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G, SkBf16>(src[c0 >> 3], qc + c0, C, acc);
       }
       if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
         const int t = tbase + i;
@@ -572,9 +574,9 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 // OR-ed into fbm.  If any check fails (region overflow, band > sel_cap, r < 0
 // or r > band, too many ties) the row is recomputed exactly the slow way into
 // a zeroed fbm row.
-template <int G>
+template <int G, class Sk>
 __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
-    const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
+    const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     BudgetDev bud, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
     const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm, int ldw,
@@ -782,9 +784,9 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     for (int w = tid; w < nw; w += kSelNT) fr[w] = 0u;
     float* sr = scratch + (size_t)row * ld;
     for (int t = tid; t < N; t += kSelNT) {
-      const uint16_t* rowp = sk + sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+      const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
       float acc = 0.f;
-      for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1>(ldg_nc_v4(rowp + c0), qc + c0, C, &acc);
+      for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1, Sk>(Sk::load8(sk, re + c0), qc + c0, C, &acc);
       sr[t] = (t < rb.lo || t >= rb.hi) ? INFINITY : acc;
     }
     __syncthreads();
@@ -864,16 +866,16 @@ int band_capacity(int max_seq_len, Budget bud) {
   return (cap + 255) & ~255;
 }
 
-template <int G>
+template <int G, class Sk>
 cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch& skc, const void* q, Budget bud,
                          const SbsBuffers& w, cudaStream_t st) {
-  const uint16_t* sk = reinterpret_cast<const uint16_t*>(skc.pages);
+  const void* sk = skc.pages;
   const int C = skc.channels;
   const int BG = geo.B * geo.Hkv;
   cudaError_t e;
   {
     const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C;
-    auto kern = sbs_sample_kernel<G>;
+    auto kern = sbs_sample_kernel<G, Sk>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
@@ -886,7 +888,8 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
                         sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * kScanMaxWords +
                         (sizeof(float) * G + sizeof(uint16_t)) * kScanWarps * kScanCandCap;
     dim3 grid(nch, BG);
-    auto kern = C == 8 ? sbs_scan_kernel<G, true> : sbs_scan_kernel<G, false>;
+    // the fp8 sketch is C = 8 only (host-checked): no generic-C fp8 variant
+    auto kern = C == 8 ? sbs_scan_kernel<G, true, Sk> : sbs_scan_kernel<G, false, SkBf16>;
     set_smem(kern, smem);
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
@@ -898,7 +901,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   {
     const int sel_cap = band_capacity(geo.max_seq_len, bud);
     const size_t smem = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
-    auto kern = sbs_select_kernel<G>;
+    auto kern = sbs_select_kernel<G, Sk>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(geo.B * geo.Hq), dim3(kSelNT), smem, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), (const uint32_t*)w.thr,
@@ -916,10 +919,14 @@ cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sket
                               const SbsBuffers& w, cudaStream_t st) {
   cudaError_t e;
   switch (g.G) {
-    case 1: e = sbs_launch_t<1>(g, kv, sk, q, bud, w, st); break;
-    case 2: e = sbs_launch_t<2>(g, kv, sk, q, bud, w, st); break;
-    case 4: e = sbs_launch_t<4>(g, kv, sk, q, bud, w, st); break;
-    case 8: e = sbs_launch_t<8>(g, kv, sk, q, bud, w, st); break;
+    case 1: e = sk.dtype == SD_E4M3 ? sbs_launch_t<1, SkE4m3>(g, kv, sk, q, bud, w, st)
+                                      : sbs_launch_t<1, SkBf16>(g, kv, sk, q, bud, w, st); break;
+    case 2: e = sk.dtype == SD_E4M3 ? sbs_launch_t<2, SkE4m3>(g, kv, sk, q, bud, w, st)
+                                      : sbs_launch_t<2, SkBf16>(g, kv, sk, q, bud, w, st); break;
+    case 4: e = sk.dtype == SD_E4M3 ? sbs_launch_t<4, SkE4m3>(g, kv, sk, q, bud, w, st)
+                                      : sbs_launch_t<4, SkBf16>(g, kv, sk, q, bud, w, st); break;
+    case 8: e = sk.dtype == SD_E4M3 ? sbs_launch_t<8, SkE4m3>(g, kv, sk, q, bud, w, st)
+                                      : sbs_launch_t<8, SkBf16>(g, kv, sk, q, bud, w, st); break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess || !w.idx_out) return e;

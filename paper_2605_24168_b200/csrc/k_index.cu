@@ -13,9 +13,9 @@ constexpr int kScanThreads = 256;
 constexpr int kScanTok = 2048;   // tokens per CTA
 
 // grid = (ceil(max_seq_len / kScanTok), B*Hkv)
-template <int G>
+template <int G, class Sk>
 __global__ void __launch_bounds__(kScanThreads) sketch_score_kernel(
-    const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk,
+    const void* __restrict__ q, int q_dtype, const void* __restrict__ sk,
     const int* __restrict__ channel_ids, int C, const int* __restrict__ page_table,
     const int* __restrict__ seq_lens, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
   extern __shared__ float qc[];  // [G][C]
@@ -36,11 +36,11 @@ __global__ void __launch_bounds__(kScanThreads) sketch_score_kernel(
   float* srow = scores + ((size_t)b * Hq + g * G) * ld;
   for (int t = tbeg + threadIdx.x; t < tend; t += kScanThreads) {
     const int page = __ldg(pt + (t >> 4));
-    const uint16_t* row = sk + sketch_row_elem(page, t & 15, g, Hkv, C);
+    const size_t row = sketch_row_elem(page, t & 15, g, Hkv, C);
     float acc[G];
 #pragma unroll
     for (int j = 0; j < G; ++j) acc[j] = 0.f;
-    for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G>(ldg_nc_v4(row + c0), qc + c0, C, acc);
+    for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G, Sk>(Sk::load8(sk, row + c0), qc + c0, C, acc);
 #pragma unroll
     for (int j = 0; j < G; ++j) srow[(size_t)j * ld + t] = acc[j];
   }
@@ -86,9 +86,14 @@ cudaError_t index_dispatch(const Geo& g, const sd_paged_kv& kv, const sd_sketch*
   dim3 grid((g.max_seq_len + kScanTok - 1) / kScanTok, g.B * g.Hkv);
   if (sk) {
     const size_t smem = sizeof(float) * G * sk->channels;
-    sketch_score_kernel<G><<<grid, kScanThreads, smem, st>>>(
-        q, g.kv_dtype, reinterpret_cast<const uint16_t*>(sk->pages), sk->channel_ids, sk->channels,
-        kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, scores, ld);
+    if (sk->dtype == SD_E4M3)
+      sketch_score_kernel<G, SkE4m3><<<grid, kScanThreads, smem, st>>>(
+          q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_pages, g.Hkv,
+          scores, ld);
+    else
+      sketch_score_kernel<G, SkBf16><<<grid, kScanThreads, smem, st>>>(
+          q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_pages, g.Hkv,
+          scores, ld);
   } else if (g.kv_dtype == SD_BF16) {
     exact_score_kernel<KvBF16, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens,
                                                                  g.max_pages, g.Hkv, scores, ld);

@@ -129,6 +129,8 @@ sd_status check_sketch(const sd_sketch* sk) {
   if (!sk->pages || !sk->channel_ids || sk->channels < 1) return SD_ERR_INVALID_ARG;
   if (sk->channels > kHeadDim) return SD_ERR_INVALID_ARG;  // C <= D
   if (sk->channels % 8) return SD_ERR_UNSUPPORTED;
+  if (sk->dtype != SD_BF16 && sk->dtype != SD_E4M3) return SD_ERR_INVALID_ARG;
+  if (sk->dtype == SD_E4M3 && sk->channels != 8) return SD_ERR_UNSUPPORTED;  // NEXT-4: the 8-channel sketch
   return SD_OK;
 }
 

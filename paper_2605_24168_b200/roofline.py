@@ -63,7 +63,7 @@ def _io(B, Hq, D, w_q, w_o):
 
 
 def sparse_step_bytes(B, Hq, Hkv, N: IntOrList, k: IntOrList, D=128, w=2, C=8, exact=False,
-                      union_rows_total: Optional[int] = None, w_o=None, page_size=16) -> dict:
+                      union_rows_total: Optional[int] = None, w_o=None, page_size=16, sketch_w=2) -> dict:
     """Per-step algorithmic bytes of the fused path; `union_rows_total` (measured
     from the selected indices) gives the must-move union model, otherwise the
     independence estimate E is used."""
@@ -72,7 +72,7 @@ def sparse_step_bytes(B, Hq, Hkv, N: IntOrList, k: IntOrList, D=128, w=2, C=8, e
     G = Hq // Hkv
     if union_rows_total is None:
         union_rows_total = int(round(sum(Hkv * expected_union(n, kk, G) for n, kk in zip(lens, ks))))
-    idx_b = indexer_bytes(B, lens, Hkv, C, 2, D, w, exact)
+    idx_b = indexer_bytes(B, lens, Hkv, C, sketch_w, D, w, exact)
     io = _io(B, Hq, D, w, w_o or w)
     pt = sum(4 * math.ceil(n / page_size) for n in lens)
     uni = gather_bytes_union(union_rows_total, D, w)

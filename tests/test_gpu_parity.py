@@ -52,6 +52,50 @@ def test_index_score_matches_oracle(cuda_lib, dtype, mode):
             assert np.all(np.abs(sc[b, h, :N] - ref) <= n * u * mag + 1e-30), (b, h)
 
 
+def test_index_score_fp8_sketch_matches_oracle(cuda_lib):
+    """NEXT-4: the e4m3 sketch is converted exactly, so the scores meet the same
+    fp32 error bound against the oracle's fp64 sum of the same e4m3 values."""
+    sd = cuda_lib
+    lens = [33, 4099, 9000]
+    case = workloads.make_case(len(lens), 16, 4, lens, seed=13, sketch_dtype=torch.float8_e4m3fn)
+    inp = oracle.from_case(case)
+    dc = _dev(case)
+    kv, sk = _kv(sd, dc)
+    sc = sd.sparse_index_score(dc.q, kv, sk).cpu().double().numpy()
+    u = 2.0 ** -24
+    for b, N in enumerate(lens):
+        for h in range(16):
+            ref = oracle.index_scores(inp, b, h, "sketch")
+            g = h // 4
+            mag = np.abs(inp.sketch(b, g)) @ np.abs(inp.q[b, h][inp.channel_ids[b, g]])
+            assert np.all(np.abs(sc[b, h, :N] - ref) <= 8 * u * mag + 1e-30), (b, h)
+
+
+@pytest.mark.parametrize("dist", ["iid", "needle", "dup"])
+def test_fused_fp8_sketch_matches_oracle(cuda_lib, dist):
+    """NEXT-4 through the fused entry: selection against the oracle's scores of
+    the same e4m3 sketch, outputs against attend_given on the selection."""
+    lens = [20000, 4099, 300]
+    case = workloads.make_case(len(lens), 32, 8, lens, seed=19, dist=dist, n_needles=32,
+                               sketch_dtype=torch.float8_e4m3fn)
+    _check_fused(cuda_lib, case, 50.0, "sketch")
+
+
+def test_fused_fp8_equals_unfused_chain(cuda_lib):
+    """The fp8-sketch fused step selects exactly what sd_sparse_index_score ->
+    sd_topk_select select on the same e4m3 sketch."""
+    sd = cuda_lib
+    case = _dev(workloads.make_case(2, 32, 8, [30000, 777], seed=43, dist="needle", n_needles=40,
+                                    sketch_dtype=torch.float8_e4m3fn))
+    kv, sk = _kv(sd, case)
+    _, _, idx_f, cnt_f = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, return_idx=True)
+    scores = sd.sparse_index_score(case.q, kv, sk)
+    idx_u, cnt_u = sd.topk_select(scores, case.seq_lens, int(case.seq_lens.max()), S=50.0, num_kv_heads=8)
+    assert torch.equal(cnt_f, cnt_u)
+    k = idx_u.shape[-1]
+    assert torch.equal(idx_f[..., :k], idx_u)
+
+
 # --------------------------------------------------------------------------- A3
 def _seeded_scores(B, H, lens, seed, kind):
     g = torch.Generator().manual_seed(seed)

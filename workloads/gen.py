@@ -99,7 +99,8 @@ def _token_rows(page_table_row: torch.Tensor, toks: torch.Tensor, ps: int):
 def make_case(B: int, Hq: int, Hkv: int, seq_lens: Union[int, Sequence[int]], *, D: int = 128,
               page_size: int = 16, C: int = 8, dtype: torch.dtype = torch.bfloat16,
               seed: int = 0, dist: str = "iid", n_needles: int = 0, nu: float = 3.0,
-              sketch: bool = True, spare_pages: int = 0, device="cpu") -> DecodeCase:
+              sketch: bool = True, spare_pages: int = 0, device="cpu",
+              sketch_dtype: torch.dtype = torch.bfloat16) -> DecodeCase:
     if Hq % Hkv:
         raise ValueError("Hq must be a multiple of Hkv")
     if isinstance(seq_lens, int):
@@ -178,6 +179,10 @@ def make_case(B: int, Hq: int, Hkv: int, seq_lens: Union[int, Sequence[int]], *,
             kp = k_pages[p0:p1].permute(0, 2, 1, 3)                      # [n, Hkv, ps, D]
             idx = ch[:, :, None, :].expand(p1 - p0, Hkv, ps, C)
             sketch_pages[p0:p1] = torch.gather(kp, 3, idx).to(torch.bfloat16)
+        if sketch_dtype != torch.bfloat16:
+            # NEXT-4 low-precision sketch: the same channels
+            # rounded to the storage type (fp8 e4m3: round to nearest, |x| <= 448)
+            sketch_pages = sketch_pages.to(sketch_dtype)
 
     return DecodeCase(B=B, Hq=Hq, Hkv=Hkv, D=D, page_size=ps, C=C,
                       seq_lens=torch.tensor(seq_lens, dtype=torch.int32, device=device),
@@ -197,6 +202,9 @@ CONFIGS = {
     "cfg2_s50": dict(B=8, Hq=32, Hkv=8, N=32768, S=50.0, dtype=torch.bfloat16, sketch=True),
     "cfg2_s100": dict(B=8, Hq=32, Hkv=8, N=32768, S=100.0, dtype=torch.bfloat16, sketch=True),
     "cfg3": dict(B=16, Hq=32, Hkv=8, N=131072, S=50.0, dtype=torch.bfloat16, sketch=True),
+    # NEXT-4: cfg3 with the 8-channel sketch stored as fp8 e4m3 (half the indexer bytes)
+    "cfg3_fp8": dict(B=16, Hq=32, Hkv=8, N=131072, S=50.0, dtype=torch.bfloat16, sketch=True,
+                     sketch_dtype=torch.float8_e4m3fn),
     "cfg4_t66": dict(B=32, Hq=32, Hkv=8, N=_cfg4_len(66), S=50.0, dtype=torch.bfloat16, sketch=True),
     "cfg4_t33": dict(B=32, Hq=32, Hkv=8, N=_cfg4_len(33), S=50.0, dtype=torch.bfloat16, sketch=True),
     "cfg4_t0": dict(B=32, Hq=32, Hkv=8, N=_cfg4_len(0), S=50.0, dtype=torch.bfloat16, sketch=True),
@@ -211,4 +219,4 @@ def config_case(name: str, *, seed: Optional[int] = None, device="cpu", **over) 
         seed = 1000 * (list(CONFIGS).index(name) + 1)
     return make_case(c["B"], c["Hq"], c["Hkv"], c["N"], dtype=c["dtype"], sketch=c["sketch"],
                      seed=seed, device=device,
-                     **{k: v for k, v in c.items() if k in ("dist", "n_needles", "nu", "C")})
+                     **{k: v for k, v in c.items() if k in ("dist", "n_needles", "nu", "C", "sketch_dtype")})
