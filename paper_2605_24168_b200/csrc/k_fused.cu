@@ -207,21 +207,14 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
-  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSampleThreads);
-  for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist1[i] = 0;
-  for (int i = tid; i < G * 512; i += kSampleThreads) hist2[i] = 0;
-  if (tid == 0) {
-    counters[bg] = 0;                   // re-arm the gather-attend merge counter of (b, g)
-    if (bg == 0) counters[gridDim.x] = 0;  // and the work counter
-  }
-  __syncthreads();
-  if (N < 1) return;
-  const int npg = (N + 15) >> 4;
+  // the sample's sketch rows first (N -> page ids -> rows is the longest
+  // dependent chain); the q channels, the histogram clearing and the barrier
+  // overlap with those loads
+  const int npg = (max(N, 1) + 15) >> 4;
   const int cap_pages = CAP >> 4;
   const int spg = (npg + cap_pages - 1) / cap_pages;  // page stride
   const int ns_pages = (npg + spg - 1) / spg;
   const int n_slots = ns_pages * 16;
-  // all loads of this thread first (latency-bound gather of sample pages)
   typename Sk::Raw raw[kSampleSlots];
   int tt[kSampleSlots];
 #pragma unroll
@@ -231,6 +224,15 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     tt[u] = (i < n_slots && t < N) ? t : -1;
     if (tt[u] >= 0) raw[u] = Sk::load8(sk, sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
+  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSampleThreads);
+  for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist1[i] = 0;
+  for (int i = tid; i < G * 512; i += kSampleThreads) hist2[i] = 0;
+  if (tid == 0) {
+    counters[bg] = 0;                   // re-arm the gather-attend merge counter of (b, g)
+    if (bg == 0) counters[gridDim.x] = 0;  // and the work counter
+  }
+  __syncthreads();
+  if (N < 1) return;
   const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
   const int k = min(rbud.k, N);
   uint32_t key[kSampleSlots][G];
@@ -283,6 +285,12 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   }
   __syncthreads();
   // level 2: the next 8 key bits inside the two bins of each head
+  int bin_lo[G], bin_hi[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    bin_lo[j] = s_bin1[j][0];
+    bin_hi[j] = s_bin1[j][1];
+  }
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
     if (tt[u] < 0) continue;
@@ -290,8 +298,8 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     for (int j = 0; j < G; ++j) {
       const int b1 = (int)(key[u][j] >> kSampleSh1);
       const uint32_t b2 = (key[u][j] >> kSampleSh2) & 255u;
-      if (b1 == s_bin1[j][0]) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
-      if (b1 == s_bin1[j][1]) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+      if (b1 == bin_lo[j]) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
+      if (b1 == bin_hi[j]) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
     }
   }
   __syncthreads();
