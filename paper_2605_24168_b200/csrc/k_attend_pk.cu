@@ -80,6 +80,15 @@ __device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a2, uin
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+// D = A(16x16, row) * B(16x8, col) + D with all four A registers
+__device__ __forceinline__ void mma_bf16_full(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                              uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -232,7 +241,9 @@ __global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
   const int qr = lane >> 2, qc2 = (lane & 3) * 2;
   const int lr = lane & 7, lm = lane >> 3;
   uint32_t qa0[8], qa2[8];
-  float o[16][4];
+  // O^T accumulators: m-tile mt covers dims [16 mt, 16 mt + 16); lane (g, t)
+  // holds O[head 2t][dim g], O[head 2t+1][dim g], O[head 2t][dim g+8], O[head 2t+1][dim g+8]
+  float oT[8][4];
   float m = -INFINITY, lsum = 0.f;
 
   for (;;) {
@@ -248,7 +259,7 @@ __global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
         }
       }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
       m = -INFINITY;
       lsum = 0.f;
     }
@@ -320,10 +331,15 @@ __global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
           const float mn = grow ? tmax : m;
           const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
           lsum *= corr;
+          // this lane's O^T columns are heads 2t, 2t+1: their factors live in lanes 8t, 8t + 4
+          const float ca = __shfl_sync(0xffffffffu, corr, (lane & 3) * 8);
+          const float cb = __shfl_sync(0xffffffffu, corr, (lane & 3) * 8 + 4);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            o[i][0] *= corr;
-            o[i][1] *= corr;
+          for (int i = 0; i < 8; ++i) {
+            oT[i][0] *= ca;
+            oT[i][1] *= cb;
+            oT[i][2] *= ca;
+            oT[i][3] *= cb;
           }
           m = mn;
         }
@@ -334,15 +350,15 @@ __global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
         const uint32_t ph0 = pack_bf16(p[0], p[1]), ph2 = pack_bf16(p[2], p[3]);
         const uint32_t pl0 = pack_bf16(p[0] - bf16_round(p[0]), p[1] - bf16_round(p[1]));
         const uint32_t pl2 = pack_bf16(p[2] - bf16_round(p[2]), p[3] - bf16_round(p[3]));
+        // O^T += V^T P^T: A = V^T tile (16 dims x 16 tokens, ldmatrix.trans of
+        // the token-major rows), B = P^T = the S fragments of this lane as they are
 #pragma unroll
-        for (int nd = 0; nd < 16; nd += 2) {
-          const int r = (lm & 1) * 8 + lr, c = nd + (lm >> 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(vb + swz(r, c), b0, b1, b2, b3);
-          mma_bf16(o[nd], ph0, ph2, b0, b1);
-          mma_bf16(o[nd], pl0, pl2, b0, b1);
-          mma_bf16(o[nd + 1], ph0, ph2, b2, b3);
-          mma_bf16(o[nd + 1], pl0, pl2, b2, b3);
+        for (int mt = 0; mt < 8; ++mt) {
+          const int r = (lm >> 1) * 8 + lr, c = 2 * mt + (lm & 1);
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(vb + swz(r, c), a0, a1, a2, a3);
+          mma_bf16_full(oT[mt], a0, a1, a2, a3, ph0, ph2);
+          mma_bf16_full(oT[mt], a0, a1, a2, a3, pl0, pl2);
         }
       }
       ++computed;
@@ -360,10 +376,21 @@ __global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
       float ls = lsum;
       ls += __shfl_xor_sync(0xffffffffu, ls, 1);
       ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-      if (qr < G) {
+      {
+        const int h0 = qc2, h1 = qc2 + 1;  // this lane's two heads (2t, 2t+1)
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          *reinterpret_cast<float2*>(&st_o[(warp * G + qr) * kD + i * 8 + qc2]) = make_float2(o[i][0], o[i][1]);
+        for (int i = 0; i < 8; ++i) {
+          if (h0 < G) {
+            st_o[(warp * G + h0) * kD + 16 * i + qr] = oT[i][0];
+            st_o[(warp * G + h0) * kD + 16 * i + qr + 8] = oT[i][2];
+          }
+          if (h1 < G) {
+            st_o[(warp * G + h1) * kD + 16 * i + qr] = oT[i][1];
+            st_o[(warp * G + h1) * kD + 16 * i + qr + 8] = oT[i][3];
+          }
+        }
+      }
+      if (qr < G) {
         if ((lane & 3) == 0) {
           st_m[warp * G + qr] = m;
           st_l[warp * G + qr] = ls;
