@@ -205,6 +205,96 @@ def union_rows(idx, counts, Hkv):
     return int((new & (s >= 0)).sum().item())
 
 
+def run_seqshard(args, world, rank, dev):
+    """BASELINE cfg5: one 2^20-token sequence, sequence-sharded over the ranks
+    (SURVEY.md 8(e)): local top-k_b candidates with k_b from the GLOBAL length,
+    all-gather of candidate scores, the global cut, local attend, all-gather of
+    the normalised partials, LSE merge (paper_2605_24168_b200.parallel)."""
+    import torch
+    import torch.distributed as dist
+    import workloads
+    import paper_2605_24168_b200 as sd
+    from paper_2605_24168_b200 import parallel as par
+    from paper_2605_24168_b200 import roofline as RL
+
+    cfg = dict(workloads.CONFIGS["cfg5"])
+    NG, S = cfg["N"], cfg["S"]
+    bounds = par.token_bounds(NG, world)
+    n_loc = bounds[rank + 1] - bounds[rank]
+    case = workloads.make_case(1, cfg["Hq"], cfg["Hkv"], n_loc, dtype=cfg["dtype"], sketch=True,
+                               seed=9000 + rank, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(4242)  # the query is the same on every rank
+    qs = [torch.randn(case.q.shape, generator=g, device=dev).to(case.q.dtype) for _ in range(4)]
+    kv = sd.KVCache.from_case(case)
+    sk = sd.SketchCache.from_case(case)
+    glens = torch.tensor([NG], dtype=torch.int32, device=dev)
+    k = sd.budget_k(S, NG)
+
+    def step(q):
+        backend = par.CudaSeqShardBackend(q, kv, sk)
+        return par.seqshard_decode(backend, glens, NG, S, SCALE, k)
+
+    for i in range(args.warmup):
+        step(qs[i % 4])
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for i in range(args.steps):
+        step(qs[i % 4])
+    ev1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    # end to end: the query from pinned host memory, the merged output back
+    q_host = torch.stack([q.cpu() for q in qs]).pin_memory()
+    out_host = torch.empty(case.q.shape, dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(qs[0])
+    dist.barrier()
+    ev0.record()
+    for i in range(args.steps):
+        q_dev.copy_(q_host[i % 4], non_blocking=True)
+        o, _ = step(q_dev)
+        out_host.copy_(o, non_blocking=True)
+    ev1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_e2e = float(t.item()) / args.steps
+    hbm, src = peaks()
+    # per-rank algorithmic bytes: the shard's sketch + the rows of its survivors (<= k)
+    model = RL.sparse_step_bytes(1, cfg["Hq"], cfg["Hkv"], n_loc, min(k, n_loc), union_rows_total=None)
+    achieved = model["total_union"] / (ms_step * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": 1000.0 / ms_step, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"cfg5: B=1, N={NG}, S={S:g}, Hq=32, Hkv=8, D=128, page 16, bf16 KV, sketch "
+                                   f"C=8 bf16; sequence-sharded over {world} GPUs ({n_loc} tokens per rank)",
+                       "global_batch": 1, "seq_len": NG, "sparsity": S, "k": k, "parallelism": f"seq-shard{world}",
+                       "l2": "per-rank inputs 600+ MB > L2, 4 rotating queries"},
+            "us_per_step": ms_step * 1e3,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "peak_source": src,
+                         "kernel": "per-rank step (local scan + top-k + cut + attend; the independence bound on "
+                                   "the rows a rank attends)", "algorithmic_bytes_per_launch": model["total_union"]},
+            "e2e": {"value": 1000.0 / ms_e2e, "unit": "tokens/s", "h2d_bytes_per_step": qs[0].numel() * 2,
+                    "d2h_bytes_per_step": out_host.numel() * 4},
+            "gpu_launches": None, "clocks": clocks,
+            "note": "exchange: two all-gathers per step (candidate scores, normalised partials) over "
+                    + dist.get_backend()}))
+    dist.barrier()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -243,6 +333,8 @@ def main():
         else:
             dist.init_process_group(backend)
     sd.load_library()
+    if args.config == "cfg5" and world > 1:
+        return run_seqshard(args, world, rank, dev)
 
     case, cfg = rank_case(args.config, world, rank, dev)
     S = cfg["S"]

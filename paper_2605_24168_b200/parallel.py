@@ -51,8 +51,10 @@ def all_gather_stack(t: torch.Tensor, group=None) -> torch.Tensor:
     """[P, *t.shape] in rank order."""
     world = dist.get_world_size(group)
     out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-    if t.is_cuda:
+    if t.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    elif t.is_cuda:  # a CPU backend (gloo) with device tensors: stage through the host
+        return all_gather_stack(t.cpu(), group).to(t.device)
     else:
         parts = list(out.unbind(0))
         dist.all_gather(parts, t.contiguous(), group=group)
