@@ -467,6 +467,36 @@ def test_fused_baseline_sizes_sampled_rows(cuda_lib, name):
             check_lse(float(lse[b, h]), rl)
 
 
+@pytest.mark.parametrize("N,expect_fast", [(1 << 20, True), ((1 << 21) - 8192, None), ((1 << 21) + 4096, False)])
+def test_fused_maximum_lengths(cuda_lib, N, expect_fast):
+    """The fused path at the longest sequences: 2^20 (BASELINE cfg5 on one GPU,
+    fast path), the last length whose band-region table fits the select's
+    shared memory (2^21 - 8192: the 4096-token sample's bracket is then wider
+    than the band capacity for most rows, which take the exact slow path), and
+    beyond it (every row on the slow path).  Same results either way; sampled
+    rows checked one by one against the oracle."""
+    sd = cuda_lib
+    case = workloads.make_case(1, 8, 2, [N], seed=81, dist="needle", n_needles=16, device="cuda")
+    kv, sk = _kv(sd, case)
+    sd.clear_device_error()
+    out, lse, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk, S=100.0, scale=SCALE, out_dtype=torch.float32,
+                                                return_idx=True)
+    torch.cuda.synchronize()
+    assert sd.read_device_error() == 0
+    fb = sd.read_stats()["fallback_rows"]
+    if expect_fast is not None:
+        assert (fb == 0) if expect_fast else (fb == case.Hq), fb
+    sub = host_subcase(case, 0)
+    inp = oracle.from_case(sub)
+    k = oracle.budget_k(100.0, N)
+    for h in (0, 5):
+        scores = oracle.index_scores(inp, 0, h, "sketch")
+        sel = check_selection(idx[0, h].cpu().numpy(), int(cnt[0, h]), scores, k)
+        ro, rl = oracle.attend_given(inp, 0, h, sel, SCALE)
+        assert rel_err(out[0, h].cpu().numpy(), ro) <= 1e-4
+        check_lse(float(lse[0, h]), rl)
+
+
 # --------------------------------------------------------------------------- sequence sharding (1 GPU)
 def _shard_kv(sd, case, lo, hi):
     """KV cache view of tokens [lo, hi) of every sequence (lo page-aligned)."""
