@@ -29,6 +29,7 @@
 //
 // Deterministic: no float atomics; union rows are rebuilt in token order.
 #include <limits.h>
+#include <stdlib.h>
 #include <math.h>
 
 #include <algorithm>
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
-    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud) {
+    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud, int xexp) {
   constexpr int NW = kScanNT / 32;
   static_assert(NW == kScanWarps, "one band region per scan warp");
   constexpr int CW = band_region_cap(G);
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   int* s_pages = reinterpret_cast<int*>(qc + G * C);                                // [kRangeTok / 16]
   uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pages + kRangeTok / 16);        // [G][kScanMaxWords]
   float* c_sc_all = reinterpret_cast<float*>(s_words + G * kScanMaxWords);          // [NW][kScanCandCap][G]
-  uint16_t* c_tok_all = reinterpret_cast<uint16_t*>(c_sc_all + NW * G * kScanCandCap);  // [NW][kScanCandCap]
+  uint16_t* c_tok_all = reinterpret_cast<uint16_t*>(c_sc_all + NW * G * kScanCandCap);  // [NW][2 kScanCandCap]
 
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
@@ -400,7 +401,11 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int t0 = chunk * kRangeTok;
   const size_t reg = ((size_t)bg * nch + chunk) * NW + warp;
   if (t0 >= N) {
-    if (lane == 0) ent_cnt[reg] = 0;
+    if (C8 && SkMma<G, Sk>::value) {
+      if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
+    } else if (lane == 0) {
+      ent_cnt[reg] = 0;
+    }
     pdl_launch_dependents();
     return;
   }
@@ -455,8 +460,12 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 #pragma unroll
   for (int s = 0; s < kScanStages - 1; ++s) issue(s);
 
+  constexpr bool kMma = C8 && SkMma<G, Sk>::value;  // tensor-core scores (sd_score.cuh)
   float qr[G][8];
-  if (C8) {
+  SkMmaQ qm;
+  if constexpr (kMma) {
+    qm = sk_mma_q([qc](int j, int c) { return qc[j * 8 + c]; }, q_dtype == SD_F32 ? 3 : 1);
+  } else if (C8) {
 #pragma unroll
     for (int j = 0; j < G; ++j)
 #pragma unroll
@@ -482,6 +491,15 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   uint32_t* fw = fbm + (size_t)(row0 + (own_j < G ? own_j : 0)) * ldw;
   int wc = 0;
   int slot_out = 0;  // ring slot of the stage being scored
+  // kMma: this lane's head pair p = u & 1 (phase 1); the thresholds of both pairs (phase 2)
+  int wc1 = 0;  // kMma: band entries of pair 1 (wc: pair 0)
+  const int pm_r = lane >> 2, pm_u = lane & 3, pm_p = pm_u & 1;
+  const float pm_fla0 = flo[0], pm_fla1 = flo[G > 1 ? 1 : 0], pm_flb0 = flo[G > 2 ? 2 : 0], pm_flb1 = flo[G > 3 ? 3 : 0];
+  const float pm_fsa0 = fsure[0], pm_fsa1 = fsure[G > 1 ? 1 : 0], pm_fsb0 = fsure[G > 2 ? 2 : 0],
+              pm_fsb1 = fsure[G > 3 ? 3 : 0];
+  const float pm_fl0 = pm_p ? pm_flb0 : pm_fla0, pm_fl1 = pm_p ? pm_flb1 : pm_fla1;
+  float2* pm_c2 = reinterpret_cast<float2*>(c_sc_all) + warp * 2 * kScanCandCap;  // [2 * kScanCandCap]
+  uint16_t* pm_ct = c_tok_all + warp * 2 * kScanCandCap;
 
   for (int s = 0; s < nst; ++s) {
     issue(s + kScanStages - 1);
@@ -496,6 +514,43 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     if (lane < G * nown) s_words[own_j * kScanMaxWords + own_w] = 0u;
     // ---- phase 1: score every token; keep the candidates (key >= lo for some head)
     int wn = 0;
+    if constexpr (kMma) {
+      // one MMA per 32-token block (sd_score.cuh): lane (r, u) holds heads 2p,
+      // 2p+1 (p = u & 1) of tokens tA, tA + 8; each (token, pair) with a score
+      // >= lo becomes a candidate: its 2 scores and token | p << 15
+#pragma unroll 4
+      for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
+        const int blk = i0 + warp * 32;
+        uint32_t a[4];
+        sk_mma_a_smem(a, smem_u32(st + (size_t)blk * 16));
+        float d[4];
+        sk_mma_score(a, qm, d);
+        if (xexp == 3) {
+          wn += __float_as_int(d[0] + d[1] + d[2] + d[3]) == 12345 ? 1 : 0;
+          continue;
+        }
+        const int tA = blk + pm_r + ((pm_u >> 1) << 4), tB = tA + 8;
+        if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
+          if (tbase + tA < rb.lo || tbase + tA >= rb.hi) d[0] = d[1] = INFINITY;
+          if (tbase + tB < rb.lo || tbase + tB >= rb.hi) d[2] = d[3] = INFINITY;
+        }
+        const bool cA = tA < lim && (d[0] >= pm_fl0 || d[1] >= pm_fl1);
+        const bool cB = tB < lim && (d[2] >= pm_fl0 || d[3] >= pm_fl1);
+        const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
+        const int nA = __popc(bA);
+        if (cA) {
+          const int p = wn + __popc(bA & lt_mask);
+          pm_c2[p] = make_float2(d[0], d[1]);
+          pm_ct[p] = (uint16_t)(tA | (pm_p << 15));
+        }
+        if (cB) {
+          const int p = wn + nA + __popc(bB & lt_mask);
+          pm_c2[p] = make_float2(d[2], d[3]);
+          pm_ct[p] = (uint16_t)(tB | (pm_p << 15));
+        }
+        wn += nA + __popc(bB);
+      }
+    } else {
 #pragma unroll 4
     for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
       const int i = i0 + tid;  // token within the stage
@@ -538,9 +593,37 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
       }
       wn += __popc(cb);
     }
+    }
     __syncwarp();
     // ---- phase 2: classify the candidates, one per lane: sure bits into the
     // stage words (shared-memory atomics), band tokens into the region
+    if constexpr (kMma) {
+      if (xexp == 4) wn = 0;
+      for (int c0 = 0; c0 < wn; c0 += 32) {
+        const int ci = c0 + lane;
+        const bool have = ci < wn;
+        const uint32_t code = have ? (uint32_t)pm_ct[ci] : 0u;
+        const float2 v = have ? pm_c2[ci] : make_float2(-INFINITY, -INFINITY);
+        const int i = (int)(code & 0x7FFFu), p = (int)(code >> 15);
+        const bool s0 = v.x >= (p ? pm_fsb0 : pm_fsa0), s1 = v.y >= (p ? pm_fsb1 : pm_fsa1);
+        uint32_t* sw = s_words + (2 * p) * kScanMaxWords + (i >> 5);
+        if (s0) atomicOr(sw, 1u << (i & 31));
+        if (s1) atomicOr(sw + kScanMaxWords, 1u << (i & 31));
+        const uint32_t m = (!s0 && v.x >= (p ? pm_flb0 : pm_fla0) ? 1u : 0u) |
+                           (!s1 && v.y >= (p ? pm_flb1 : pm_fla1) ? 2u : 0u);
+        const uint32_t b0 = __ballot_sync(0xffffffffu, m && !p), b1 = __ballot_sync(0xffffffffu, m && p);
+        if (m) {
+          const int pos = (p ? wc1 : wc) + __popc((p ? b1 : b0) & lt_mask);
+          if (pos < CW) {
+            const size_t e = (reg * 2 + p) * CW + pos;
+            ent_tok[e] = (uint32_t)(tbase + i) | (m << 24);
+            reinterpret_cast<float2*>(ent_sc)[e] = v;
+          }
+        }
+        wc += __popc(b0);
+        wc1 += __popc(b1);
+      }
+    } else {
     for (int c0 = 0; c0 < wn; c0 += 32) {
       const int ci = c0 + lane;
       const bool have = ci < wn;
@@ -564,13 +647,21 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         wc += __popc(bb);
       }
     }
+    }
     __syncwarp();
     // ---- this warp's words of the stage -> the G rows' selection bitmaps
     if (lane < G * nown && own_w * 32 < lim) fw[(tbase >> 5) + own_w] = s_words[own_j * kScanMaxWords + own_w];
     __syncthreads();  // slot reuse by the next issue()
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (lane == 0) ent_cnt[reg] = wc;
+  if (kMma) {
+    if (lane == 0) {
+      ent_cnt[reg * 2 + 0] = wc;
+      ent_cnt[reg * 2 + 1] = wc1;
+    }
+  } else if (lane == 0) {
+    ent_cnt[reg] = wc;
+  }
   pdl_launch_dependents();
 }
 
@@ -582,7 +673,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 // OR-ed into fbm.  If any check fails (region overflow, band > sel_cap, r < 0
 // or r > band, too many ties) the row is recomputed exactly the slow way into
 // a zeroed fbm row.
-template <int G, class Sk>
+template <int G, class Sk, bool Pair>
 __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
@@ -648,12 +739,18 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     if (tid == 0) s_fb = 1;
   }
   const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t jbit = 1u << (24 + j);
+  // band regions: union format (one per scan warp, G scores per entry) or, on
+  // the tensor-core scan (Pair), one per (scan warp, head pair) with the
+  // pair's 2 scores per entry
+  constexpr int nsub = Pair ? 2 : 1, nh = Pair ? 2 : G;
+  const int sub = Pair ? (j >> 1) : 0, e = Pair ? (j & 1) : j;
+  const uint32_t jbit = 1u << (24 + e);
   const size_t reg0 = (size_t)bg * nch * NW;
+  auto greg = [&](int r) { return (reg0 + r) * nsub + sub; };
   // region counts -> shared memory in one coalesced pass (overflow: slow path)
   int* s_cnt = reinterpret_cast<int*>(ties);  // reuse: [nreg]
   for (int r = tid; r < nreg; r += kSelNT) {
-    int c = ent_cnt[reg0 + r];
+    int c = ent_cnt[greg(r)];
     if (c > CW) {
       s_fb = 1;
       c = 0;
@@ -685,13 +782,13 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     for (int qq = 0; qq < RQ; ++qq) {
       const int r = rb + (kSelNT / 32) * qq;
       cnt[qq] = r < nreg ? s_cnt[r] : 0;
-      const uint32_t* rtok = ent_tok + (reg0 + r) * CW;
-      const float* rsc = ent_sc + (reg0 + r) * CW * G + j;
+      const uint32_t* rtok = ent_tok + greg(r) * CW;
+      const float* rsc = ent_sc + greg(r) * CW * nh + e;
 #pragma unroll
       for (int u = 0; u < UQ; ++u) {
         const int i = lane + 32 * u;
         tk[qq][u] = i < cnt[qq] ? rtok[i] : 0u;
-        sc[qq][u] = i < cnt[qq] ? rsc[(size_t)i * G] : 0.f;
+        sc[qq][u] = i < cnt[qq] ? rsc[(size_t)i * nh] : 0.f;
       }
     }
 #pragma unroll
@@ -703,7 +800,7 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
       for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
         const int i = i0 + lane;
         const bool in = i < cnt[qq];
-        keep(in ? ent_tok[(reg0 + r) * CW + i] : 0u, in ? ent_sc[((reg0 + r) * CW + i) * G + j] : 0.f);
+        keep(in ? ent_tok[greg(r) * CW + i] : 0u, in ? ent_sc[(greg(r) * CW + i) * nh + e] : 0.f);
       }
     }
   }
@@ -791,11 +888,29 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
     if (tid == 0 && err) atomicAdd(err + 1, 1);  // statistics word: fallback rows
     for (int w = tid; w < nw; w += kSelNT) fr[w] = 0u;
     float* sr = scratch + (size_t)row * ld;
-    for (int t = tid; t < N; t += kSelNT) {
-      const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-      float acc = 0.f;
-      for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1, Sk>(Sk::load8(sk, re + c0), qc + c0, C, &acc);
-      sr[t] = (t < rb.lo || t >= rb.hi) ? INFINITY : acc;
+    if (SkMma<G, Sk>::value && C == 8) {  // the scan's tensor-core scores, same MMA placement
+      const int jh = j;
+      const SkMmaQ qm = sk_mma_q([qc, jh](int j, int c) { return j == jh ? qc[c] : 0.f; }, q_dtype == SD_F32 ? 3 : 1);
+      const int u = lane & 3, tofs = (lane >> 2) + ((u >> 1) << 4);
+      const bool mine = (u & 1) == (jh >> 1);
+      for (int t0 = warp * 32; t0 < N; t0 += kSelNT) {
+        uint32_t a[4];
+        sk_mma_a_global(a, reinterpret_cast<const uint16_t*>(sk), t0, N,
+                        [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, 8); });
+        float d[4];
+        sk_mma_score(a, qm, d);
+        const int tA = t0 + tofs, tB = tA + 8;
+        const float vA = (jh & 1) ? d[1] : d[0], vB = (jh & 1) ? d[3] : d[2];
+        if (mine && tA < N) sr[tA] = (tA < rb.lo || tA >= rb.hi) ? INFINITY : vA;
+        if (mine && tB < N) sr[tB] = (tB < rb.lo || tB >= rb.hi) ? INFINITY : vB;
+      }
+    } else {
+      for (int t = tid; t < N; t += kSelNT) {
+        const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+        float acc = 0.f;
+        for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1, Sk>(Sk::load8(sk, re + c0), qc + c0, C, &acc);
+        sr[t] = (t < rb.lo || t >= rb.hi) ? INFINITY : acc;
+      }
     }
     __syncthreads();
     auto key_at = [sr](int i) { return score_key(sr[i]); };
@@ -862,6 +977,15 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 // (sigma = sqrt(k f (1 - f)), f = sample fraction) plus the two edge bins;
 // sized at 1.5x that + 2048, within [4096, kSelCap] (4 select CTAs per SM at
 // the low end, 1 at the high end).
+static int scan_exp() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_SCAN_EXP");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 int band_capacity(int max_seq_len, Budget bud) {
   const double N = std::max(1, max_seq_len);
   const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N)
@@ -894,7 +1018,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   {
     const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 + sizeof(float) * G * C +
                         sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * kScanMaxWords +
-                        (sizeof(float) * G + sizeof(uint16_t)) * kScanWarps * kScanCandCap;
+                        (sizeof(float) * G + 2 * sizeof(uint16_t)) * kScanWarps * kScanCandCap;
     dim3 grid(nch, BG);
     // the fp8 sketch is C = 8 only (host-checked): no generic-C fp8 variant
     auto kern = C == 8 ? sbs_scan_kernel<G, true, Sk> : sbs_scan_kernel<G, false, SkBf16>;
@@ -902,14 +1026,14 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
                    geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch,
-                   bud.dev());
+                   bud.dev(), scan_exp());
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
   {
     const int sel_cap = band_capacity(geo.max_seq_len, bud);
     const size_t smem = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
-    auto kern = sbs_select_kernel<G, Sk>;
+    auto kern = (SkMma<G, Sk>::value && C == 8) ? sbs_select_kernel<G, Sk, true> : sbs_select_kernel<G, Sk, false>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(geo.B * geo.Hq), dim3(kSelNT), smem, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), (const uint32_t*)w.thr,

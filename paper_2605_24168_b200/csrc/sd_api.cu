@@ -39,12 +39,13 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
     const int G = Hq / Hkv;
     const size_t nreg = (size_t)B * Hkv * L.nrange * kScanWarps;
     const size_t cap = band_region_cap(G);
+    const size_t nsub = G == 4 ? 2 : 1;  // the tensor-core scan's per-pair regions (k_fused.cu)
     L.ent_tok = off;
-    off = align256(off + nreg * cap * sizeof(uint32_t));
+    off = align256(off + nreg * nsub * cap * sizeof(uint32_t));
     L.ent_sc = off;
     off = align256(off + nreg * cap * G * sizeof(float));
     L.ent_cnt = off;
-    off = align256(off + nreg * sizeof(int));
+    off = align256(off + nreg * nsub * sizeof(int));
     L.fbm = off;
     off = align256(off + rows * (size_t)L.ldw * sizeof(uint32_t));
   }

@@ -3,7 +3,9 @@
 //
 // Sketch mode (Double Sparsity):
 //   s_hat[t] = sum_{c < C} qc[c] * sk[t][c],  qc[c] = q[h][channel_ids[b][g][c]]
-//   evaluated as the fp32 fma chain acc = fma(qc[c], sk[c], acc), c ascending.
+//   evaluated as the fp32 fma chain acc = fma(qc[c], sk[c], acc), c ascending,
+//   except for G = 4, C = 8, bf16 sketch: one bf16 tensor-core MMA with fp32
+//   accumulation (SkMma below), the same in every kernel.
 // Exact mode (oracle top-k): s_hat[t] = <q_h, K_t>, evaluated per 16-lane
 //   half-warp: lane l sums dims [8l, 8l+8) with an fma chain, then a xor
 //   butterfly over 8, 4, 2, 1.
@@ -42,6 +44,90 @@ struct SkE4m3 {
     }
   }
 };
+
+// ---- G = 4 q-heads per KV head, C = 8, bf16 sketch: the score on the tensor
+// cores.  The indexer is the contraction [32 tokens x 8 channels] x [8 x 4 heads];
+// one mma.sync.m16n8k16 (bf16 in, fp32 accumulate) scores 32 consecutive tokens
+// t0 .. t0+31 of one warp for all 4 heads:
+//   A (16 x 16, row): A[m][k] = sk[t0 + m][k] (k < 8),  sk[t0 + 16 + m][k - 8] (k >= 8)
+//   B (16 x 8, col) : B[k][n] = q[n][k] (k < 8, n < 4),  q[n - 4][k - 8] (k >= 8, n >= 4), else 0
+//   D[m][n]         = score(token t0 + m + 16 [n >= 4], head n & 3)
+// q (fp32 in general) enters as an exact sum of bf16 parts hi + mid + lo (one
+// part when q is bf16), accumulated in that order.  Every kernel that scores
+// with this path (fused scan, select fallback, unfused indexer) starts t0 at a
+// multiple of 32 and builds the same B, so a (token, head) score is the same
+// bits everywhere.  Lane L (r = L/4, u = L%4) holds d[0], d[1] = heads 2(u&1),
+// 2(u&1)+1 of token tA = t0 + r + 16(u>>1), and d[2], d[3] = those of tA + 8.
+template <int G, class Sk>
+struct SkMma {
+  static constexpr bool value = false;
+};
+template <>
+struct SkMma<4, SkBf16> {
+  static constexpr bool value = true;
+};
+
+struct SkMmaQ {
+  uint32_t b[3][2];
+  int np;
+};
+__device__ __forceinline__ uint16_t sk_to_bf16(float v) {
+  uint16_t h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(v));
+  return h;
+}
+// qf(head, channel) -> fp32 q value (0 for heads the caller does not score);
+// np = 1 when q is bf16 (exact in one part), else 3.
+template <class QF>
+__device__ __forceinline__ SkMmaQ sk_mma_q(QF qf, int np) {
+  const int lane = threadIdx.x & 31, n = lane >> 2, u = lane & 3;
+  const int head = n & 3, grp = n >> 2;
+  float v0 = qf(head, 2 * u), v1 = qf(head, 2 * u + 1);
+  SkMmaQ r;
+  r.np = np;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const uint16_t h0 = sk_to_bf16(v0), h1 = sk_to_bf16(v1);
+    const uint32_t w = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    r.b[p][0] = grp == 0 ? w : 0u;
+    r.b[p][1] = grp == 0 ? 0u : w;
+    v0 -= __uint_as_float((uint32_t)h0 << 16);  // exact residuals
+    v1 -= __uint_as_float((uint32_t)h1 << 16);
+  }
+  return r;
+}
+__device__ __forceinline__ void sk_mma(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void sk_mma_score(const uint32_t (&a)[4], const SkMmaQ& q, float (&d)[4]) {
+  d[0] = d[1] = d[2] = d[3] = 0.f;
+  sk_mma(d, a, q.b[0]);
+  if (q.np > 1) {
+    sk_mma(d, a, q.b[1]);
+    sk_mma(d, a, q.b[2]);
+  }
+}
+// A fragment of tokens t0 .. t0+31 from 16-B rows in shared memory (row i at base + 16 i).
+__device__ __forceinline__ void sk_mma_a_smem(uint32_t (&a)[4], uint32_t base) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(base + (uint32_t)(threadIdx.x & 31) * 16u));
+}
+// A fragment from global memory: row(t) -> element offset of token t's sketch
+// row (t < n; tokens >= n contribute zero rows).
+template <class RowElem>
+__device__ __forceinline__ void sk_mma_a_global(uint32_t (&a)[4], const uint16_t* sk, int t0, int n, RowElem row) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, u = lane & 3;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int t = t0 + 8 * m + r;
+    a[m] = t < n ? __ldg(reinterpret_cast<const uint32_t*>(sk + row(t)) + u) : 0u;
+  }
+}
 
 // Sketch row address (elements) of token (page, slot) for KV head g.
 __device__ __forceinline__ size_t sketch_row_elem(int page, int slot, int g, int Hkv, int C) {
