@@ -49,7 +49,6 @@ constexpr int kSampleSlots = 8;            // sample tokens per thread (cap 4096
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
-constexpr int kScanMaxWords = kScanStageTok8 / 32;  // bitmap words per stage (C = 8: 32)
 constexpr int kScanCandCap = kScanStageTok8 / 8;    // candidates per warp per stage (<= its tokens)
 constexpr int kSelNT = 512;
 constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
@@ -135,12 +134,6 @@ __device__ __forceinline__ float thresh_lo(uint32_t lo) {
   if (lo <= 0x007FFFFFu) return -INFINITY;  // below key(-inf): every finite score
   if (lo >= 0xFF800000u) return INFINITY;   // above key(+inf): none
   return key_score(lo);
-}
-
-__device__ __forceinline__ void cp_async16_zf(void* dst, const void* src, bool valid) {
-  const uint32_t d = smem_u32(dst);
-  const int n = valid ? 16 : 0;  // 0 => zero-fill
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
 // --------------------------------------------------------------------------- 1. sample
@@ -376,21 +369,26 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
-    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud, int xexp) {
+    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud) {
   constexpr int NW = kScanNT / 32;
   static_assert(NW == kScanWarps, "one band region per scan warp");
   constexpr int CW = band_region_cap(G);
+  constexpr bool kMma = C8 && SkMma<G, Sk>::value;  // tensor-core scores (sd_score.cuh)
+  constexpr int kWords = kRangeTok / 32;              // bitmap words of the chunk, per head
+  // per-warp candidate buffer: (token, head pair) entries on the tensor-core
+  // path, (token) entries otherwise; flushed (phase 2) before a block could overflow it
+  constexpr int kCap = kMma ? 2 * kScanCandCap : kScanCandCap;
+  constexpr int kPerBlk = kMma ? 64 : 32;  // new candidates per warp per 32-token block, at most
   extern __shared__ __align__(128) unsigned char smem[];
+  const int rowb = C * Sk::kBytes;                        // one token's sketch row
   const int stage_tok = (kScanStageTok8 * 8 / C) & ~31;  // whole bitmap words per stage
-  const int stage_bytes = kScanStageTok8 * 16;  // ring slot size (bf16 rows; fp8 rows use half)
-  constexpr int kRowB = 8 * Sk::kBytes;           // C8: one token's sketch row (16 B bf16, 8 B fp8)
-  constexpr int kTpc = 16 / kRowB;                // C8: tokens per 16-B copy
+  const int stage_bytes = kScanStageTok8 * 16;            // ring slot size
   unsigned char* ring = smem;
-  float* qc = reinterpret_cast<float*>(ring + (size_t)kScanStages * stage_bytes);  // [G][C]
-  int* s_pages = reinterpret_cast<int*>(qc + G * C);                                // [kRangeTok / 16]
-  uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pages + kRangeTok / 16);        // [G][kScanMaxWords]
-  float* c_sc_all = reinterpret_cast<float*>(s_words + G * kScanMaxWords);          // [NW][kScanCandCap][G]
-  uint16_t* c_tok_all = reinterpret_cast<uint16_t*>(c_sc_all + NW * G * kScanCandCap);  // [NW][2 kScanCandCap]
+  float* qc = reinterpret_cast<float*>(ring + (size_t)kScanStages * stage_bytes);        // [G][C]
+  int* s_pages = reinterpret_cast<int*>(qc + G * C);                                      // [kRangeTok / 16]
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(s_pages + kRangeTok / 16);              // [G][kWords]
+  float* c_sc_all = reinterpret_cast<float*>(s_words + G * kWords);                       // [NW][kScanCandCap][G]
+  uint16_t* c_tok_all = reinterpret_cast<uint16_t*>(c_sc_all + NW * G * kScanCandCap);    // [NW][2 kScanCandCap]
 
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
@@ -401,7 +399,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int t0 = chunk * kRangeTok;
   const size_t reg = ((size_t)bg * nch + chunk) * NW + warp;
   if (t0 >= N) {
-    if (C8 && SkMma<G, Sk>::value) {
+    if (kMma) {
       if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
     } else if (lane == 0) {
       ent_cnt[reg] = 0;
@@ -413,18 +411,20 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int npages = (ntok + 15) >> 4;
   const int* pt = page_table + (size_t)b * max_pages;
   for (int i = tid; i < npages; i += kScanNT) s_pages[i] = __ldg(pt + (t0 >> 4) + i);
+  for (int i = tid; i < G * kWords; i += kScanNT) s_words[i] = 0u;
   load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kScanNT);
   __syncthreads();
   const int nst = (ntok + stage_tok - 1) / stage_tok;
-  const int cpt = C >> 3;  // 16-B chunks per token
-  // C8: thread tid copies tokens tid + 256 u of a stage: page (tid >> 4) + 16 u
-  // of the stage's 64, slot tid & 15 (fixed per thread)
+  const int cpt = rowb >> 4;  // 16-B chunks per token (0 for the 8-B fp8 rows)
+  // C8: thread tid copies 16-B chunk tid + 256 u of a stage (kTpc tokens each):
+  // page (tid * kTpc >> 4) + 16 kTpc u of the stage, slot (tid * kTpc) & 15
+  constexpr int kRowB = 8 * Sk::kBytes;  // C8: one token's sketch row (16 B bf16, 8 B fp8)
+  constexpr int kTpc = 16 / kRowB;       // C8: tokens per 16-B copy
   const char* tb = skb + ((size_t)g * kPS + ((tid * kTpc) & 15)) * kRowB;
   const uint32_t page_bytes = (uint32_t)Hkv * kPS * kRowB;
-  int slot_in = 0;  // ring slot of the next issue
   auto issue = [&](int s) {
     if (s < nst) {
-      unsigned char* st = ring + (size_t)slot_in * stage_bytes;
+      unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
       if (C8) {
         const int* sp = s_pages + (s * kScanStageTok8 >> 4) + ((tid * kTpc) >> 4);
         if ((s + 1) * kScanStageTok8 <= ntok) {  // full stage: plain copies
@@ -434,33 +434,33 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
             const char* src = tb + (size_t)(uint32_t)sp[u * (kScanNT * kTpc >> 4)] * page_bytes;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
           }
-        } else {  // the range's tail: rows past the end are zero-filled
+        } else {  // the range's tail: only the pages that exist (rows >= N are masked)
 #pragma unroll
           for (int u = 0; u < kScanStageTok8 / kScanNT / kTpc; ++u) {
             const int ti = tid + u * kScanNT;  // 16-B chunk: tokens kTpc ti ..
-            const bool valid = s * kScanStageTok8 + ti * kTpc < ntok;
-            const char* src = valid ? tb + (size_t)(uint32_t)sp[u * (kScanNT * kTpc >> 4)] * page_bytes : skb;
-            cp_async16_zf(st + (size_t)ti * 16, src, valid);
+            if (s * kScanStageTok8 + ti * kTpc < ntok) {
+              const uint32_t d = smem_u32(st + (size_t)ti * 16);
+              const char* src = tb + (size_t)(uint32_t)sp[u * (kScanNT * kTpc >> 4)] * page_bytes;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+            }
           }
         }
       } else {
-        const int nq = stage_tok * cpt;
+        const int nq = min(stage_tok, ntok - s * stage_tok) * cpt;
         for (int qd = tid; qd < nq; qd += kScanNT) {
           const int ti = qd / cpt, c = qd - ti * cpt;
           const int i = s * stage_tok + ti;  // chunk-relative token
-          const bool valid = i < ntok;
-          const char* src = valid ? skb + (sketch_row_elem(s_pages[i >> 4], i & 15, g, Hkv, C) + c * 8) * 2 : skb;
-          cp_async16_zf(st + (size_t)qd * 16, src, valid);
+          const char* src = skb + (sketch_row_elem(s_pages[i >> 4], i & 15, g, Hkv, C) + c * 8) * 2;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(st + (size_t)qd * 16)), "l"(src)
+                       : "memory");
         }
       }
-      slot_in = slot_in + 1 == kScanStages ? 0 : slot_in + 1;
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
   for (int s = 0; s < kScanStages - 1; ++s) issue(s);
 
-  constexpr bool kMma = C8 && SkMma<G, Sk>::value;  // tensor-core scores (sd_score.cuh)
   float qr[G][8];
   SkMmaQ qm;
   if constexpr (kMma) {
@@ -483,16 +483,12 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t* rtok = ent_tok + reg * CW;
   float* rsc = ent_sc + reg * CW * G;
-  float* c_sc = c_sc_all + warp * G * kScanCandCap;      // this warp's candidates of the stage ([p][G])
+  float* c_sc = c_sc_all + warp * G * kScanCandCap;  // this warp's candidates ([p][G])
   uint16_t* c_tok = c_tok_all + warp * kScanCandCap;
-  // bitmap words owned per stage: lane < G * nown handles head own_j, word own_w
-  const int nown = C8 ? kScanStageTok8 / kScanNT : (stage_tok + kScanNT - 1) / kScanNT;
-  const int own_j = lane / nown, own_w = (lane - own_j * nown) * NW + warp;
-  uint32_t* fw = fbm + (size_t)(row0 + (own_j < G ? own_j : 0)) * ldw;
-  int wc = 0;
-  int slot_out = 0;  // ring slot of the stage being scored
+  int wn = 0;   // candidates buffered by this warp (chunk-relative tokens)
+  int wc = 0;   // band entries written (kMma: of head pair 0)
+  int wc1 = 0;  // kMma: band entries of head pair 1
   // kMma: this lane's head pair p = u & 1 (phase 1); the thresholds of both pairs (phase 2)
-  int wc1 = 0;  // kMma: band entries of pair 1 (wc: pair 0)
   const int pm_r = lane >> 2, pm_u = lane & 3, pm_p = pm_u & 1;
   const float pm_fla0 = flo[0], pm_fla1 = flo[G > 1 ? 1 : 0], pm_flb0 = flo[G > 2 ? 2 : 0], pm_flb1 = flo[G > 3 ? 3 : 0];
   const float pm_fsa0 = fsure[0], pm_fsa1 = fsure[G > 1 ? 1 : 0], pm_fsb0 = fsure[G > 2 ? 2 : 0],
@@ -501,34 +497,86 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   float2* pm_c2 = reinterpret_cast<float2*>(c_sc_all) + warp * 2 * kScanCandCap;  // [2 * kScanCandCap]
   uint16_t* pm_ct = c_tok_all + warp * 2 * kScanCandCap;
 
+  // ---- phase 2: classify the buffered candidates, one per lane: sure bits into
+  // the chunk's words (shared-memory atomics), band tokens into the region
+  auto flush = [&]() {
+    __syncwarp();
+    if constexpr (kMma) {
+      for (int c0 = 0; c0 < wn; c0 += 32) {
+        const int ci = c0 + lane;
+        const bool have = ci < wn;
+        const uint32_t code = have ? (uint32_t)pm_ct[ci] : 0u;
+        const float2 v = have ? pm_c2[ci] : make_float2(-INFINITY, -INFINITY);
+        const int i = (int)(code & 0x7FFFu), p = (int)(code >> 15);
+        const bool s0 = v.x >= (p ? pm_fsb0 : pm_fsa0), s1 = v.y >= (p ? pm_fsb1 : pm_fsa1);
+        uint32_t* sw = s_words + (2 * p) * kWords + (i >> 5);
+        if (s0) atomicOr(sw, 1u << (i & 31));
+        if (s1) atomicOr(sw + kWords, 1u << (i & 31));
+        const uint32_t m = (!s0 && v.x >= (p ? pm_flb0 : pm_fla0) ? 1u : 0u) |
+                           (!s1 && v.y >= (p ? pm_flb1 : pm_fla1) ? 2u : 0u);
+        const uint32_t b0 = __ballot_sync(0xffffffffu, m && !p), b1 = __ballot_sync(0xffffffffu, m && p);
+        if (m) {
+          const int pos = (p ? wc1 : wc) + __popc((p ? b1 : b0) & lt_mask);
+          if (pos < CW) {
+            const size_t e = (reg * 2 + p) * CW + pos;
+            ent_tok[e] = (uint32_t)(t0 + i) | (m << 24);
+            reinterpret_cast<float2*>(ent_sc)[e] = v;
+          }
+        }
+        wc += __popc(b0);
+        wc1 += __popc(b1);
+      }
+    } else {
+      for (int c0 = 0; c0 < wn; c0 += 32) {
+        const int ci = c0 + lane;
+        const bool have = ci < wn;
+        const int i = have ? (int)c_tok[ci] : 0;
+        float sc[G];
+        uint32_t bm = 0;
+        load_scores<G>(sc, c_sc + (have ? ci : 0) * G);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (!have) sc[j] = -INFINITY;
+          if (sc[j] >= fsure[j]) atomicOr(&s_words[j * kWords + (i >> 5)], 1u << (i & 31));
+          else if (sc[j] >= flo[j]) bm |= 1u << j;
+        }
+        const uint32_t bb = __ballot_sync(0xffffffffu, bm != 0u);
+        if (bb) {
+          const int pos = wc + __popc(bb & lt_mask);
+          if (bm && pos < CW) {
+            rtok[pos] = (uint32_t)(t0 + i) | (bm << 24);
+            store_scores<G>(rsc + (size_t)pos * G, sc);
+          }
+          wc += __popc(bb);
+        }
+      }
+    }
+    __syncwarp();
+    wn = 0;
+  };
+
   for (int s = 0; s < nst; ++s) {
     issue(s + kScanStages - 1);
     asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
     __syncthreads();
-    const unsigned char* st = ring + (size_t)slot_out * stage_bytes;
-    slot_out = slot_out + 1 == kScanStages ? 0 : slot_out + 1;
-    const int lim = min(stage_tok, ntok - s * stage_tok);  // valid tokens of this stage
-    const int tbase = t0 + s * stage_tok;                  // first token of the stage
+    const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+    const int cb = s * stage_tok;                   // chunk-relative first token of the stage
+    const int lim = min(stage_tok, ntok - cb);      // valid tokens of this stage
+    const int tbase = t0 + cb;                      // first token of the stage
     const bool edge_stage = tbase < rb.lo || tbase + lim > rb.hi;  // touches the sink / local regions
-    // this warp owns bitmap words w + 8 q of the stage (the tokens it scores)
-    if (lane < G * nown) s_words[own_j * kScanMaxWords + own_w] = 0u;
     // ---- phase 1: score every token; keep the candidates (key >= lo for some head)
-    int wn = 0;
     if constexpr (kMma) {
       // one MMA per 32-token block (sd_score.cuh): lane (r, u) holds heads 2p,
       // 2p+1 (p = u & 1) of tokens tA, tA + 8; each (token, pair) with a score
       // >= lo becomes a candidate: its 2 scores and token | p << 15
 #pragma unroll 4
       for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
+        if (wn > kCap - kPerBlk) flush();
         const int blk = i0 + warp * 32;
         uint32_t a[4];
         sk_mma_a_smem(a, smem_u32(st + (size_t)blk * 16));
         float d[4];
         sk_mma_score(a, qm, d);
-        if (xexp == 3) {
-          wn += __float_as_int(d[0] + d[1] + d[2] + d[3]) == 12345 ? 1 : 0;
-          continue;
-        }
         const int tA = blk + pm_r + ((pm_u >> 1) << 4), tB = tA + 8;
         if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
           if (tbase + tA < rb.lo || tbase + tA >= rb.hi) d[0] = d[1] = INFINITY;
@@ -541,119 +589,72 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         if (cA) {
           const int p = wn + __popc(bA & lt_mask);
           pm_c2[p] = make_float2(d[0], d[1]);
-          pm_ct[p] = (uint16_t)(tA | (pm_p << 15));
+          pm_ct[p] = (uint16_t)((cb + tA) | (pm_p << 15));
         }
         if (cB) {
           const int p = wn + nA + __popc(bB & lt_mask);
           pm_c2[p] = make_float2(d[2], d[3]);
-          pm_ct[p] = (uint16_t)(tB | (pm_p << 15));
+          pm_ct[p] = (uint16_t)((cb + tB) | (pm_p << 15));
         }
         wn += nA + __popc(bB);
       }
     } else {
 #pragma unroll 4
-    for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
-      const int i = i0 + tid;  // token within the stage
-      const bool valid = i < lim;
-      float acc[G];
+      for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
+        if (wn > kCap - kPerBlk) flush();
+        const int i = i0 + tid;  // token within the stage
+        const bool valid = i < lim;
+        float acc[G];
 #pragma unroll
-      for (int j = 0; j < G; ++j) acc[j] = 0.f;
-      if (C8) {
-        float x[8];
-        Sk::unpack(*reinterpret_cast<const typename Sk::Raw*>(st + (size_t)(i < stage_tok ? i : 0) * kRowB), x);
+        for (int j = 0; j < G; ++j) acc[j] = 0.f;
+        if (C8) {
+          float x[8];
+          Sk::unpack(*reinterpret_cast<const typename Sk::Raw*>(st + (size_t)(i < stage_tok ? i : 0) * rowb), x);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (G == 1) {
-            acc[0] = fmaf(qr[0][c], x[c], acc[0]);
-          } else {
+          for (int c = 0; c < 8; ++c) {
+            if (G == 1) {
+              acc[0] = fmaf(qr[0][c], x[c], acc[0]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < G; j += 2) ffma2(acc[j], acc[j + 1], qr[j][c], qr[j + 1][c], x[c]);
+              for (int j = 0; j < G; j += 2) ffma2(acc[j], acc[j + 1], qr[j][c], qr[j + 1][c], x[c]);
+            }
+          }
+        } else if (i < stage_tok) {
+          const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
+          for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G, SkBf16>(src[c0 >> 3], qc + c0, C, acc);
+        }
+        if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
+          const int t = tbase + i;
+          if (t < rb.lo || t >= rb.hi) {
+#pragma unroll
+            for (int j = 0; j < G; ++j) acc[j] = INFINITY;
           }
         }
-      } else if (i < stage_tok) {
-        const uint4* src = reinterpret_cast<const uint4*>(st + (size_t)i * 2 * C);
-        for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<G, SkBf16>(src[c0 >> 3], qc + c0, C, acc);
-      }
-      if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
-        const int t = tbase + i;
-        if (t < rb.lo || t >= rb.hi) {
+        bool cand = false;
 #pragma unroll
-          for (int j = 0; j < G; ++j) acc[j] = INFINITY;
+        for (int j = 0; j < G; ++j) cand |= acc[j] >= flo[j];
+        cand &= valid;
+        const uint32_t cbal = __ballot_sync(0xffffffffu, cand);
+        if (cand) {
+          const int p = wn + __popc(cbal & lt_mask);
+          c_tok[p] = (uint16_t)(cb + i);
+          store_scores<G>(c_sc + p * G, acc);
         }
-      }
-      bool cand = false;
-#pragma unroll
-      for (int j = 0; j < G; ++j) cand |= acc[j] >= flo[j];
-      cand &= valid;
-      const uint32_t cb = __ballot_sync(0xffffffffu, cand);
-      if (cand) {
-        const int p = wn + __popc(cb & lt_mask);
-        c_tok[p] = (uint16_t)i;
-        store_scores<G>(c_sc + p * G, acc);
-      }
-      wn += __popc(cb);
-    }
-    }
-    __syncwarp();
-    // ---- phase 2: classify the candidates, one per lane: sure bits into the
-    // stage words (shared-memory atomics), band tokens into the region
-    if constexpr (kMma) {
-      if (xexp == 4) wn = 0;
-      for (int c0 = 0; c0 < wn; c0 += 32) {
-        const int ci = c0 + lane;
-        const bool have = ci < wn;
-        const uint32_t code = have ? (uint32_t)pm_ct[ci] : 0u;
-        const float2 v = have ? pm_c2[ci] : make_float2(-INFINITY, -INFINITY);
-        const int i = (int)(code & 0x7FFFu), p = (int)(code >> 15);
-        const bool s0 = v.x >= (p ? pm_fsb0 : pm_fsa0), s1 = v.y >= (p ? pm_fsb1 : pm_fsa1);
-        uint32_t* sw = s_words + (2 * p) * kScanMaxWords + (i >> 5);
-        if (s0) atomicOr(sw, 1u << (i & 31));
-        if (s1) atomicOr(sw + kScanMaxWords, 1u << (i & 31));
-        const uint32_t m = (!s0 && v.x >= (p ? pm_flb0 : pm_fla0) ? 1u : 0u) |
-                           (!s1 && v.y >= (p ? pm_flb1 : pm_fla1) ? 2u : 0u);
-        const uint32_t b0 = __ballot_sync(0xffffffffu, m && !p), b1 = __ballot_sync(0xffffffffu, m && p);
-        if (m) {
-          const int pos = (p ? wc1 : wc) + __popc((p ? b1 : b0) & lt_mask);
-          if (pos < CW) {
-            const size_t e = (reg * 2 + p) * CW + pos;
-            ent_tok[e] = (uint32_t)(tbase + i) | (m << 24);
-            reinterpret_cast<float2*>(ent_sc)[e] = v;
-          }
-        }
-        wc += __popc(b0);
-        wc1 += __popc(b1);
-      }
-    } else {
-    for (int c0 = 0; c0 < wn; c0 += 32) {
-      const int ci = c0 + lane;
-      const bool have = ci < wn;
-      const int i = have ? (int)c_tok[ci] : 0;
-      float sc[G];
-      uint32_t bm = 0;
-      load_scores<G>(sc, c_sc + (have ? ci : 0) * G);
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        if (!have) sc[j] = -INFINITY;
-        if (sc[j] >= fsure[j]) atomicOr(&s_words[j * kScanMaxWords + (i >> 5)], 1u << (i & 31));
-        else if (sc[j] >= flo[j]) bm |= 1u << j;
-      }
-      const uint32_t bb = __ballot_sync(0xffffffffu, bm != 0u);
-      if (bb) {
-        const int pos = wc + __popc(bb & lt_mask);
-        if (bm && pos < CW) {
-          rtok[pos] = (uint32_t)(tbase + i) | (bm << 24);
-          store_scores<G>(rsc + (size_t)pos * G, sc);
-        }
-        wc += __popc(bb);
+        wn += __popc(cbal);
       }
     }
-    }
-    __syncwarp();
-    // ---- this warp's words of the stage -> the G rows' selection bitmaps
-    if (lane < G * nown && own_w * 32 < lim) fw[(tbase >> 5) + own_w] = s_words[own_j * kScanMaxWords + own_w];
-    __syncthreads();  // slot reuse by the next issue()
+    __syncthreads();  // every warp is done with the slot before issue() refills it
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  flush();
+  __syncthreads();
+  // ---- the chunk's selection words (sure bits) -> the G rows' bitmaps: every
+  // word below N_b is written, so fbm needs no zeroing
+  const int nwv = (ntok + 31) >> 5;
+  for (int i = tid; i < G * kWords; i += kScanNT) {
+    const int j = i / kWords, w = i - j * kWords;
+    if (w < nwv) fbm[(size_t)(row0 + j) * ldw + (t0 >> 5) + w] = s_words[i];
+  }
   if (kMma) {
     if (lane == 0) {
       ent_cnt[reg * 2 + 0] = wc;
@@ -977,15 +978,6 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 // (sigma = sqrt(k f (1 - f)), f = sample fraction) plus the two edge bins;
 // sized at 1.5x that + 2048, within [4096, kSelCap] (4 select CTAs per SM at
 // the low end, 1 at the high end).
-static int scan_exp() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SD_SCAN_EXP");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 int band_capacity(int max_seq_len, Budget bud) {
   const double N = std::max(1, max_seq_len);
   const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N)
@@ -1016,8 +1008,8 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   }
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
   {
-    const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 + sizeof(float) * G * C +
-                        sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * kScanMaxWords +
+    const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 +
+                        sizeof(float) * G * C + sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * (kRangeTok / 32) +
                         (sizeof(float) * G + 2 * sizeof(uint16_t)) * kScanWarps * kScanCandCap;
     dim3 grid(nch, BG);
     // the fp8 sketch is C = 8 only (host-checked): no generic-C fp8 variant
@@ -1026,7 +1018,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
                    geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch,
-                   bud.dev(), scan_exp());
+                   bud.dev());
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
