@@ -24,8 +24,10 @@
 // O += (P_hi + P_lo) V; the arithmetic is that of attend_rows_mma_kernel.
 // At an item's last unit the 4 warps' states are merged (scratch: the ring
 // slot just consumed, which the cursor has not refilled yet) into the item's
-// split partial; the CTA completing the last split of a (b, g) merges the
-// splits in split order (deterministic) into out / lse.
+// split partial; merge_parts_kernel (PDL) merges the splits in split order
+// (deterministic) into out / lse.  Folding that merge into the last CTA of
+// each (b, g) needs a gpu-scope fence per item (MEMBAR.ALL.GPU + CCTL.IVALL),
+// which drains the ring's in-flight copies: measured 122 -> 240 us at cfg3.
 #include "sd_common.cuh"
 #include "sd_internal.h"
 #include "sd_sbs.cuh"

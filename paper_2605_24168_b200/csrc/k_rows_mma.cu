@@ -405,12 +405,6 @@ cudaError_t launch_mma_g(const Geo& g, const sd_paged_kv& kv, const void* q, con
 
 }  // namespace
 
-cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                                   float scale, float* part, void* out, float* lse, int* counters,
-                                   cudaStream_t st) {
-  return launch_mma_g<false>(g, kv, q, fbm, ldw, scale, part, 0, out, lse, counters, st);
-}
-
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
                                   int splits, void* out, float* lse, int* counters, cudaStream_t st) {
   return launch_mma_g<true>(g, kv, q, nullptr, 0, scale, part, splits, out, lse, counters, st);

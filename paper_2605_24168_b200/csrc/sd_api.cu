@@ -363,17 +363,7 @@ sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sk
   SD_CUDA(launch_sbs_select(g, *kv, *sketch, q, bud, w, st));
   if (g.kv_dtype == SD_BF16)
   {
-    // union gather-attend variant (A/B switch for measurements): pk (default,
-    // persistent, + split merge kernel), rows (one CTA per range, merge folded)
-    const char* v = getenv("SD_UNION_ATTEND");
-    if (v && !strcmp(v, "rows")) {
-      SD_CUDA(launch_attend_rows_mma(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st));
-      if (ev) {
-        cudaEventRecord(ev[4], st);
-        cudaEventRecord(ev[5], st);
-      }
-      return cuda_status(cudaGetLastError());
-    }
+    // persistent union gather-attend; the split merge is folded into its last CTA per (b, g)
     SD_CUDA(launch_attend_union_pk(g, *kv, q, w.fbm, w.ldw, scale, part, out, lse, w.counters, st,
                                    ev ? ev[4] : nullptr));
     if (ev) cudaEventRecord(ev[5], st);

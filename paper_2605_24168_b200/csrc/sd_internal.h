@@ -127,11 +127,8 @@ cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* 
                                float scale, float* part, int splits, cudaStream_t st);
 cudaError_t launch_dense_rows(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
                               int splits, cudaStream_t st);
-// bf16 tensor-core variants fold the split merge into their last CTA per (b, g)
+// the bf16 tensor-core dense kernel folds the split merge into their last CTA per (b, g)
 // (counters: int32 [B*Hkv], zero between calls)
-cudaError_t launch_attend_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                                   float scale, float* part, void* out, float* lse, int* counters,
-                                   cudaStream_t st);
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
                                   int splits, void* out, float* lse, int* counters, cudaStream_t st);
 // persistent variant (k_attend_pk.cu); the split partials are merged by a
