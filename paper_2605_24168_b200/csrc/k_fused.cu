@@ -44,8 +44,8 @@ namespace sd {
 namespace {
 
 constexpr float kBracketZ = 4.0f;
-constexpr int kSampleThreads = 512;
-constexpr int kSampleSlots = 8;            // sample tokens per thread (cap 4096)
+constexpr int kSampleThreads = 1024;
+constexpr int kSampleSlots = 4;            // sample tokens per thread (cap 4096)
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
