@@ -50,7 +50,7 @@ constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
 constexpr int kScanCandCap = kScanStageTok8 / 8;    // candidates per warp per stage (<= its tokens)
-constexpr int kSelNT = 512;
+constexpr int kSelNT = 256;           // 4 CTAs per SM: B*Hq = 512 rows in one wave
 constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
 constexpr int kTieCap = 2048;
 
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 // or r > band, too many ties) the row is recomputed exactly the slow way into
 // a zeroed fbm row.
 template <int G, class Sk, bool Pair>
-__global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
+__global__ void __launch_bounds__(kSelNT, 4) sbs_select_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     BudgetDev bud, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
@@ -689,8 +689,13 @@ __global__ void __launch_bounds__(kSelNT) sbs_select_kernel(
   uint32_t* toks = keys + sel_cap;                       // [sel_cap]
   uint32_t* ties = toks + sel_cap;                       // [kTieCap]
   float* qc = reinterpret_cast<float*>(ties + kTieCap);  // [C]
-  __shared__ SelectSmem<kSelNT> sm;
-  __shared__ uint32_t hist2[kHistWords];
+  // the slow path's radix state and the fast path's band histogram share storage
+  __shared__ union SelShared {
+    SelectSmem<kSelNT> sel;
+    uint32_t hist2[kHistWords];
+  } ush;
+  SelectSmem<kSelNT>& sm = ush.sel;
+  uint32_t* hist2 = ush.hist2;
   __shared__ int s_fb, s_sure, s_ntie, s_n;
   __shared__ uint32_t s_pre, s_need;
   __shared__ int s_shift, s_prev, s_done;
@@ -976,7 +981,7 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 // Shared-memory band capacity of the select kernel.  The band holds the tokens
 // between the two sample order statistics: about (2 z sigma + 2) / f tokens
 // (sigma = sqrt(k f (1 - f)), f = sample fraction) plus the two edge bins;
-// sized at 1.5x that + 2048, within [4096, kSelCap] (4 select CTAs per SM at
+// sized at 1.25x that + 1024, within [4096, kSelCap] (4 select CTAs per SM at
 // the low end, 1 at the high end).
 int band_capacity(int max_seq_len, Budget bud) {
   const double N = std::max(1, max_seq_len);
@@ -986,7 +991,7 @@ int band_capacity(int max_seq_len, Budget bud) {
   const double f = std::min(1.0, (double)(kSampleThreads * kSampleSlots) / N);
   const double sig = std::sqrt(k * f * (1.0 - f));
   const double band = (2.0 * kBracketZ * sig + 2.0) / f;
-  const int cap = (int)std::min<double>(kSelCap, std::max(4096.0, 1.5 * band + 2048.0));
+  const int cap = (int)std::min<double>(kSelCap, std::max(4096.0, 1.25 * band + 1024.0));
   return (cap + 255) & ~255;
 }
 
