@@ -33,6 +33,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "sd_common.cuh"
 #include "sd_internal.h"
@@ -127,6 +128,15 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, 
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(xx), "l"(yy), "l"(a));
   a0 = __uint_as_float((uint32_t)r);
   a1 = __uint_as_float((uint32_t)(r >> 32));
+}
+
+// Predicated candidate store (no branch): {x, y} -> *c2, code -> *ct when p.
+__device__ __forceinline__ void st_cand_pred(bool p, float2* c2, float x, float y, uint16_t* ct, uint16_t code) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
+      "@q st.shared.v2.f32 [%1], {%2, %3};\n\t@q st.shared.u16 [%4], %5;\n}" ::"r"((int)p),
+      "r"(smem_u32(c2)), "f"(x), "f"(y), "r"(smem_u32(ct)), "h"(code)
+      : "memory");
 }
 
 // Float threshold equivalent to key(s) >= lo on finite scores.
@@ -568,35 +578,52 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     if constexpr (kMma) {
       // one MMA per 32-token block (sd_score.cuh): lane (r, u) holds heads 2p,
       // 2p+1 (p = u & 1) of tokens tA, tA + 8; each (token, pair) with a score
-      // >= lo becomes a candidate: its 2 scores and token | p << 15
+      // >= lo becomes a candidate: its 2 scores and token | p << 15.  NP = the
+      // q parts of sk_mma_q (1: bf16 q); FULL = a whole stage with no sink /
+      // local tokens (no per-token range checks).
+      auto phase1 = [&](auto np_tag, auto full_tag) {
+        constexpr int NP = decltype(np_tag)::value;
+        constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll 4
-      for (int i0 = 0; i0 < stage_tok; i0 += kScanNT) {
-        if (wn > kCap - kPerBlk) flush();
-        const int blk = i0 + warp * 32;
-        uint32_t a[4];
-        sk_mma_a_smem(a, smem_u32(st + (size_t)blk * 16));
-        float d[4];
-        sk_mma_score(a, qm, d);
-        const int tA = blk + pm_r + ((pm_u >> 1) << 4), tB = tA + 8;
-        if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
-          if (tbase + tA < rb.lo || tbase + tA >= rb.hi) d[0] = d[1] = INFINITY;
-          if (tbase + tB < rb.lo || tbase + tB >= rb.hi) d[2] = d[3] = INFINITY;
+        for (int i0 = 0; i0 < kScanStageTok8; i0 += kScanNT) {
+          if (wn > kCap - kPerBlk) flush();
+          const int blk = i0 + warp * 32;
+          uint32_t a[4];
+          sk_mma_a_smem(a, smem_u32(st + (size_t)blk * 16));
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+          sk_mma(d, a, qm.b[0]);  // the accumulation order of sk_mma_score
+          if constexpr (NP > 1) {
+            sk_mma(d, a, qm.b[1]);
+            sk_mma(d, a, qm.b[2]);
+          }
+          const int tA = blk + pm_r + ((pm_u >> 1) << 4), tB = tA + 8;
+          if constexpr (!FULL) {
+            if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
+              if (tbase + tA < rb.lo || tbase + tA >= rb.hi) d[0] = d[1] = INFINITY;
+              if (tbase + tB < rb.lo || tbase + tB >= rb.hi) d[2] = d[3] = INFINITY;
+            }
+          }
+          bool cA = d[0] >= pm_fl0 || d[1] >= pm_fl1;
+          bool cB = d[2] >= pm_fl0 || d[3] >= pm_fl1;
+          if constexpr (!FULL) {
+            cA = cA && tA < lim;
+            cB = cB && tB < lim;
+          }
+          const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
+          const int nA = __popc(bA);
+          const int pA = wn + __popc(bA & lt_mask), pB = wn + nA + __popc(bB & lt_mask);
+          st_cand_pred(cA, pm_c2 + pA, d[0], d[1], pm_ct + pA, (uint16_t)((cb + tA) | (pm_p << 15)));
+          st_cand_pred(cB, pm_c2 + pB, d[2], d[3], pm_ct + pB, (uint16_t)((cb + tB) | (pm_p << 15)));
+          wn += nA + __popc(bB);
         }
-        const bool cA = tA < lim && (d[0] >= pm_fl0 || d[1] >= pm_fl1);
-        const bool cB = tB < lim && (d[2] >= pm_fl0 || d[3] >= pm_fl1);
-        const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
-        const int nA = __popc(bA);
-        if (cA) {
-          const int p = wn + __popc(bA & lt_mask);
-          pm_c2[p] = make_float2(d[0], d[1]);
-          pm_ct[p] = (uint16_t)((cb + tA) | (pm_p << 15));
-        }
-        if (cB) {
-          const int p = wn + nA + __popc(bB & lt_mask);
-          pm_c2[p] = make_float2(d[2], d[3]);
-          pm_ct[p] = (uint16_t)((cb + tB) | (pm_p << 15));
-        }
-        wn += nA + __popc(bB);
+      };
+      const bool full = lim == kScanStageTok8 && !edge_stage;
+      if (qm.np == 1) {
+        if (full) phase1(std::integral_constant<int, 1>{}, std::true_type{});
+        else phase1(std::integral_constant<int, 1>{}, std::false_type{});
+      } else {
+        if (full) phase1(std::integral_constant<int, 3>{}, std::true_type{});
+        else phase1(std::integral_constant<int, 3>{}, std::false_type{});
       }
     } else {
 #pragma unroll 4
