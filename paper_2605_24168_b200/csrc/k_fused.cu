@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(kSelNT, 4) sbs_select_kernel(
   __syncthreads();
   // warp per region with RQ regions in flight: entries lane + 32 u (u < UQ) of
   // each are loaded before any is used; longer regions finish in a tail loop
-  constexpr int RQ = 4, UQ = 4;
+  constexpr int RQ = 4, UQ = 2;
   auto keep = [&](uint32_t tk, float scv) {
     const bool c = (tk & jbit) != 0u;
     const uint32_t bal = __ballot_sync(0xffffffffu, c);
@@ -824,10 +824,33 @@ __global__ void __launch_bounds__(kSelNT, 4) sbs_select_kernel(
         sc[qq][u] = i < cnt[qq] ? rsc[(size_t)i * nh] : 0.f;
       }
     }
+    // one shared-memory atomic per warp for all RQ x UQ groups (entries past a
+    // region's count were loaded as token 0 with no head bit)
+    uint32_t bal[RQ][UQ];
+    int tot = 0;
 #pragma unroll
     for (int qq = 0; qq < RQ; ++qq)
 #pragma unroll
-      for (int u = 0; u < UQ; ++u) keep(tk[qq][u], sc[qq][u]);
+      for (int u = 0; u < UQ; ++u) {
+        bal[qq][u] = __ballot_sync(0xffffffffu, (tk[qq][u] & jbit) != 0u);
+        tot += __popc(bal[qq][u]);
+      }
+    if (tot) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_n, tot);
+      base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+      for (int qq = 0; qq < RQ; ++qq)
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) {
+          const int p = base + __popc(bal[qq][u] & lt);
+          if ((tk[qq][u] & jbit) && p < sel_cap) {
+            keys[p] = score_key(sc[qq][u]);
+            toks[p] = tk[qq][u] & 0x00FFFFFFu;
+          }
+          base += __popc(bal[qq][u]);
+        }
+    }
     for (int qq = 0; qq < RQ; ++qq) {
       const int r = rb + (kSelNT / 32) * qq;
       for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
