@@ -404,10 +404,33 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int Hq = Hkv * G;
   const int row0 = b * Hq + g * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int N = __ldg(seq_lens + b);
   const int chunk = blockIdx.x;
   const int t0 = chunk * kRangeTok;
   const size_t reg = ((size_t)bg * nch + chunk) * NW + warp;
+  // ---- prologue: every global input is requested before anything waits on
+  // one (N_b, the chunk's page ids, the channel ids, the G q rows, then the
+  // brackets once the sample kernel has finished), so the CTA start costs one
+  // memory round trip instead of four
+  const int qb = q_dtype == SD_F32 ? 4 : 2;
+  const int N = __ldg(seq_lens + b);
+  const int* pt = page_table + (size_t)b * max_pages + (t0 >> 4);
+  const int np_max = min(kRangeTok / 16, max_pages - (t0 >> 4));  // page ids past N_b are never used
+  constexpr int kPgPerThr = kRangeTok / 16 / kScanNT;
+  int pgv[kPgPerThr];
+#pragma unroll
+  for (int u = 0; u < kPgPerThr; ++u) pgv[u] = tid + u * kScanNT < np_max ? __ldg(pt + tid + u * kScanNT) : 0;
+  const int chv = tid < C ? __ldg(channel_ids + (size_t)bg * C + tid) : 0;
+  const int nq16 = G * kD * qb / 16;  // the group's q rows in 16-B pieces
+  const uint4* qsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)row0 * kD * qb);
+  uint4 qv[(8 * kD * 4 / 16 + kScanNT - 1) / kScanNT];
+#pragma unroll
+  for (int u = 0; u < (int)(sizeof(qv) / sizeof(uint4)); ++u)
+    if (tid + u * kScanNT < nq16) qv[u] = __ldg(qsrc + tid + u * kScanNT);
+  for (int i = tid; i < G * kWords; i += kScanNT) s_words[i] = 0u;
+  pdl_wait();  // the bracket comes from the sample kernel
+  uint2 thv[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) thv[j] = __ldg(reinterpret_cast<const uint2*>(thr) + row0 + j);
   if (t0 >= N) {
     if (kMma) {
       if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
@@ -418,12 +441,20 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     return;
   }
   const int ntok = min(N - t0, kRangeTok);
-  const int npages = (ntok + 15) >> 4;
-  const int* pt = page_table + (size_t)b * max_pages;
-  for (int i = tid; i < npages; i += kScanNT) s_pages[i] = __ldg(pt + (t0 >> 4) + i);
-  for (int i = tid; i < G * kWords; i += kScanNT) s_words[i] = 0u;
-  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kScanNT);
+  // the q rows and channel ids are staged in the candidate area (unused until phase 1)
+  unsigned char* s_qrow = reinterpret_cast<unsigned char*>(c_sc_all);        // [G][kD] q dtype
+  int* s_ch = reinterpret_cast<int*>(s_qrow + (size_t)G * kD * 4);            // [C]
+#pragma unroll
+  for (int u = 0; u < kPgPerThr; ++u) s_pages[tid + u * kScanNT] = pgv[u];
+  if (tid < C) s_ch[tid] = chv;
+#pragma unroll
+  for (int u = 0; u < (int)(sizeof(qv) / sizeof(uint4)); ++u)
+    if (tid + u * kScanNT < nq16) reinterpret_cast<uint4*>(s_qrow)[tid + u * kScanNT] = qv[u];
   __syncthreads();
+  auto qf = [&](int j, int c) {  // q[b][g G + j][channel_ids[b][g][c]]
+    const int e = j * kD + s_ch[c];
+    return qb == 4 ? reinterpret_cast<const float*>(s_qrow)[e] : bf_lo(reinterpret_cast<const uint16_t*>(s_qrow)[e]);
+  };
   const int nst = (ntok + stage_tok - 1) / stage_tok;
   const int cpt = rowb >> 4;  // 16-B chunks per token (0 for the 8-B fp8 rows)
   // C8: thread tid copies 16-B chunk tid + 256 u of a stage (kTpc tokens each):
@@ -474,19 +505,21 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   float qr[G][8];
   SkMmaQ qm;
   if constexpr (kMma) {
-    qm = sk_mma_q([qc](int j, int c) { return qc[j * 8 + c]; }, q_dtype == SD_F32 ? 3 : 1);
+    qm = sk_mma_q(qf, q_dtype == SD_F32 ? 3 : 1);
   } else if (C8) {
 #pragma unroll
     for (int j = 0; j < G; ++j)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) qr[j][c] = qc[j * 8 + c];
+      for (int c = 0; c < 8; ++c) qr[j][c] = qf(j, c);
+  } else {
+    for (int i = tid; i < G * C; i += kScanNT) qc[i] = qf(i / C, i - (i / C) * C);
   }
-  pdl_wait();  // the bracket comes from the sample kernel
+  __syncthreads();  // the staged q rows are read; the candidate area is free
   const RowBudget rb = row_budget(N, bud);
   float flo[G], fsure[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    const uint2 th = __ldg(reinterpret_cast<const uint2*>(thr) + row0 + j);
+    const uint2 th = thv[j];
     flo[j] = thresh_lo(th.x);
     fsure[j] = th.y == 0xFFFFFFFFu ? INFINITY : thresh_lo(th.y + 1u);  // key > hi  <=>  s >= fsure
   }
