@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   static_assert(NW == kScanWarps, "one band region per scan warp");
   constexpr int CW = band_region_cap(G);
   constexpr bool kMma = C8 && SkMma<G, Sk>::value;  // tensor-core scores (sd_score.cuh)
+  constexpr bool kWarpLocal = C8 && Sk::kBytes == 2;  // stage rows copied by the warp that scores them
   constexpr int kWords = kRangeTok / 32;              // bitmap words of the chunk, per head
   // per-warp candidate buffer: (token, head pair) entries on the tensor-core
   // path, (token) entries otherwise; flushed (phase 2) before a block could overflow it
@@ -601,7 +602,11 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   for (int s = 0; s < nst; ++s) {
     issue(s + kScanStages - 1);
     asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
-    __syncthreads();
+    // bf16 rows at C = 8: thread tid copies tokens tid + 256 u of a stage, which
+    // are exactly the 32-token blocks its warp scores, so a warp only waits for
+    // its own lanes' copies (no CTA barrier per stage); otherwise the CTA syncs
+    if constexpr (kWarpLocal) __syncwarp();
+    else __syncthreads();
     const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
     const int cb = s * stage_tok;                   // chunk-relative first token of the stage
     const int lim = min(stage_tok, ntok - cb);      // valid tokens of this stage
@@ -703,7 +708,9 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         wn += __popc(cbal);
       }
     }
-    __syncthreads();  // every warp is done with the slot before issue() refills it
+    // every lane (warp-local staging) / warp is done with the slot before issue() refills it
+    if constexpr (kWarpLocal) __syncwarp();
+    else __syncthreads();
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   flush();
