@@ -441,6 +441,396 @@ __global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
   pdl_launch_dependents();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised variant (default): 8 warps per CTA, 2 CTAs per SM.
+// Warps 4-7 (producers, 56 registers after setmaxnreg.dec) resolve work units
+// and stream their K/V rows into the ring with cp.async, signalling each stage
+// on full[slot] with cp.async.mbarrier.arrive.noinc (the arrive fires when the
+// thread's copies have landed); warps 0-3 (consumers, 200 registers) wait on
+// full[slot], compute, and release the slot on empty[slot].  Units are handed
+// over through double-buffered row lists with ready[buf] / freed[buf]
+// mbarriers.  No CTA-wide barrier in the steady state: the copy issue never
+// waits for the compute (tools/gather_ws.cu: 6.0 TB/s vs 5.5 TB/s for the
+// barrier-synchronised ring at this shape).
+constexpr int kWsThreads = 256;
+constexpr int kWsConsRegs = 200, kWsProdRegs = 56;
+
+template <int G>
+struct WsSmem {
+  unsigned char ring[kPkStages][kPkStageBytes];
+  uint32_t rowi[2][kPkBatch];
+  uint8_t rmask[2][kPkBatch];
+  uint16_t qs[2][G * kD];
+  int u_it[2], u_nrows[2], u_last[2], u_r0[2];
+  int wtot[kPkWarps];
+  uint64_t full[kPkStages], empty[kPkStages], ready[2], freed[2];
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
+    const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int n_items) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  WsSmem<G>& sm = *reinterpret_cast<WsSmem<G>*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Hq = Hkv * G;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kPkStages; ++s) {
+      mbar_init(&sm.full[s], kPkThreads);  // one noinc arrive per producer thread
+      mbar_init(&sm.empty[s], kPkWarps);   // one arrive per consumer warp
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.ready[b], 1);
+      mbar_init(&sm.freed[b], kPkWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if ((int)blockIdx.x >= n_items) {
+    pdl_launch_dependents();
+    return;
+  }
+  pdl_wait();  // selection bitmaps come from sbs_select_kernel
+
+  if (warp >= kPkWarps) {
+    // =================================================================== producers
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsProdRegs));
+    const int pt_ = tid - kPkThreads, pw = pt_ >> 5;  // producer thread / warp index
+    struct ItemRegs {
+      int it, N;
+      uint2 wv[G];
+      int pv[4];
+      uint4 qv;
+    };
+    auto load_item = [&](ItemRegs& r, int it) {
+      r.it = it;
+      if (it >= n_items) return;
+      const int bg = it / splits, split = it - bg * splits;
+      const int b = bg / Hkv, g = bg - b * Hkv;
+      r.N = __ldg(seq_lens + b);
+      const int t0 = split * kPkItemTok;
+      const int w0 = (t0 >> 5) + 2 * pt_;
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        r.wv[j] = w0 < ldw ? *reinterpret_cast<const uint2*>(fbm + (size_t)(b * Hq + g * G + j) * ldw + w0)
+                           : make_uint2(0u, 0u);
+      const int p0 = (t0 >> 4) + 4 * pt_;
+      const int* pt = page_table + (size_t)b * max_pages;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r.pv[k] = p0 + k < max_pages ? __ldg(pt + p0 + k) : 0;
+      if (pt_ < G * 16)
+        r.qv = *reinterpret_cast<const uint4*>(q + (size_t)(b * Hq + g * G + (pt_ >> 4)) * kD + (pt_ & 15) * 8);
+    };
+    // rows [r0, r0 + kPkBatch) of the item in r -> buffer buf; returns the
+    // item's union row count (producer threads only, 2 named barriers)
+    auto resolve = [&](const ItemRegs& r, int r0, int buf) -> int {
+      const int it = r.it;
+      const int bg = it / splits, split = it - bg * splits;
+      const int g = bg - (bg / Hkv) * Hkv;
+      const int T0 = min(r.N, split * kPkItemTok), ntok = min(r.N, T0 + kPkItemTok) - T0;
+      const int nw = (ntok + 31) >> 5;
+      const int w0 = 2 * pt_;
+      if (r0 == 0 && pt_ < G * 16) *reinterpret_cast<uint4*>(&sm.qs[buf][(pt_ >> 4) * kD + (pt_ & 15) * 8]) = r.qv;
+      uint32_t u0 = 0, u1 = 0;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        u0 |= w0 < nw ? r.wv[j].x : 0u;
+        u1 |= w0 + 1 < nw ? r.wv[j].y : 0u;
+      }
+      const int cnt = __popc(u0) + __popc(u1);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) sm.wtot[pw] = incl;
+      named_sync(1, kPkThreads);
+      int pos = incl - cnt, total = 0;
+#pragma unroll
+      for (int w = 0; w < kPkWarps; ++w) {
+        const int t = sm.wtot[w];
+        pos += w < pw ? t : 0;
+        total += t;
+      }
+      if (pos < r0 + kPkBatch && pos + cnt > r0) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          uint32_t x = e ? u1 : u0;
+          while (x) {
+            const int bit = __ffs(x) - 1;
+            x &= x - 1;
+            if (pos >= r0 && pos < r0 + kPkBatch) {
+              uint32_t mk = 0;
+#pragma unroll
+              for (int j = 0; j < G; ++j) {
+                const uint32_t wj = e ? (w0 + 1 < nw ? r.wv[j].y : 0u) : (w0 < nw ? r.wv[j].x : 0u);
+                mk |= ((wj >> bit) & 1u) << j;
+              }
+              const int pg = bit < 16 ? r.pv[2 * e] : r.pv[2 * e + 1];
+              sm.rowi[buf][pos - r0] = (uint32_t)(pg * kPS + (bit & 15)) * (uint32_t)Hkv + g;
+              sm.rmask[buf][pos - r0] = (uint8_t)mk;
+            }
+            ++pos;
+          }
+        }
+      }
+      named_sync(1, kPkThreads);  // wtot reusable; the buffer is complete
+      return total;
+    };
+    // hand unit u (item it, rows [r0, r0 + nrows), last-of-item flag) to the consumers
+    auto publish = [&](int u, int it, int r0, int nrows, int last) {
+      const int buf = u & 1;
+      if (pt_ == 0) {
+        sm.u_it[buf] = it;
+        sm.u_r0[buf] = r0;
+        sm.u_nrows[buf] = nrows;
+        sm.u_last[buf] = last;
+        mbar_arrive(&sm.ready[buf]);  // release: the row lists and queries above are visible
+      }
+    };
+    const int ic16 = pt_ & 15, ir0 = pt_ >> 4;
+    const char* kpc = kp + ic16 * 16;
+    const char* vpc = vp + ic16 * 16;
+    int issued = 0;
+    auto issue = [&](int buf, int stage, int nrows) {
+      const int slot = issued % kPkStages;
+      if (issued >= kPkStages) mbar_wait(&sm.empty[slot], (uint32_t)((issued / kPkStages) - 1) & 1u);
+      const uint32_t kd = smem_u32(&sm.ring[slot][0]);
+      const uint32_t vd = kd + kPkStageRows * kPkRowB;
+      const int R0 = stage * kPkStageRows;
+      const int nr = min(kPkStageRows, nrows - R0);
+      const int nr16 = (nr + 15) & ~15;  // rows of partial tiles are zero-filled
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = ir0 + 8 * i;
+        if (rr < nr16) {
+          const bool valid = rr < nr;
+          const size_t off = valid ? (size_t)sm.rowi[buf][R0 + rr] * kPkRowB : 0;
+          const uint32_t d = (uint32_t)(rr * kPkRowB + ((ic16 ^ (rr & 7)) << 4));
+          cp_async16_pk(kd + d, kpc + off, valid);
+          cp_async16_pk(vd + d, vpc + off, valid);
+        }
+      }
+      cp_async_arrive_noinc(&sm.full[slot]);
+      ++issued;
+    };
+
+    ItemRegs cur_r, nxt_r;
+    int it_c = blockIdx.x, r0_c = 0;
+    load_item(cur_r, it_c);
+    int total_c = resolve(cur_r, 0, 0);
+    load_item(nxt_r, it_c + gridDim.x);
+    int u = 0;
+    int nrows_c = min(kPkBatch, total_c);
+    publish(0, it_c, 0, nrows_c, r0_c + kPkBatch >= total_c);
+    for (;;) {
+      const int buf = u & 1;
+      const int nst = max(1, (nrows_c + kPkStageRows - 1) / kPkStageRows);
+      for (int s = 0; s < nst; ++s) issue(buf, s, nrows_c);
+      // next unit: the rest of this item, or the next item
+      int it_n, r0_n;
+      if (r0_c + kPkBatch < total_c) {
+        it_n = it_c;
+        r0_n = r0_c + kPkBatch;
+      } else {
+        it_n = nxt_r.it;
+        r0_n = 0;
+      }
+      const int nb = buf ^ 1;
+      if (u >= 1) mbar_wait(&sm.freed[nb], (uint32_t)(((u + 1) >> 1) - 1) & 1u);  // consumers done with unit u - 1
+      if (it_n >= n_items) {
+        publish(u + 1, n_items, 0, 0, 0);  // end marker
+        break;
+      }
+      int total_n;
+      if (r0_n) {
+        total_n = resolve(cur_r, r0_n, nb);
+      } else {
+        total_n = resolve(nxt_r, 0, nb);
+        cur_r = nxt_r;
+        load_item(nxt_r, it_n + gridDim.x);
+      }
+      const int nrows_n = min(kPkBatch, total_n - r0_n);
+      publish(u + 1, it_n, r0_n, nrows_n, r0_n + kPkBatch >= total_n);
+      it_c = it_n;
+      r0_c = r0_n;
+      total_c = total_n;
+      nrows_c = nrows_n;
+      ++u;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+    // =================================================================== consumers
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsConsRegs));
+    const int qr = lane >> 2, qc2 = (lane & 3) * 2;
+    const int lr = lane & 7, lm = lane >> 3;
+    uint32_t qa0[8], qa2[8];
+    float oT[8][4];
+    float m = -INFINITY, lsum = 0.f;
+    int consumed = 0;
+    for (int u = 0;; ++u) {
+      const int buf = u & 1;
+      mbar_wait(&sm.ready[buf], (uint32_t)(u >> 1) & 1u);
+      const int it_c = sm.u_it[buf];
+      if (it_c >= n_items) break;
+      const int r0_c = sm.u_r0[buf], nrows_c = sm.u_nrows[buf], last_c = sm.u_last[buf];
+      if (r0_c == 0) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          qa0[kk] = qa2[kk] = 0u;
+          if (qr < G) {
+            const uint16_t* qrow = &sm.qs[buf][qr * kD + kk * 16 + qc2];
+            qa0[kk] = *reinterpret_cast<const uint32_t*>(qrow);
+            qa2[kk] = *reinterpret_cast<const uint32_t*>(qrow + 8);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
+        m = -INFINITY;
+        lsum = 0.f;
+      }
+      const int nst = max(1, (nrows_c + kPkStageRows - 1) / kPkStageRows);
+      int slot = 0;
+      for (int cc = 0; cc < nst; ++cc) {
+        slot = consumed % kPkStages;
+        mbar_wait(&sm.full[slot], (uint32_t)(consumed / kPkStages) & 1u);
+        const unsigned char* st = sm.ring[slot];
+        const uint8_t* msk = sm.rmask[buf] + cc * kPkStageRows;
+        const int nr = min(kPkStageRows, nrows_c - cc * kPkStageRows);
+        const int trow = warp * kPkTile;
+        if (trow < nr) {
+          const uint32_t kb = smem_u32(st) + trow * kPkRowB;
+          const uint32_t vb = smem_u32(st + kPkStageRows * kPkRowB) + trow * kPkRowB;
+          float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int r = (lm >> 1) * 8 + lr, c = 2 * kk + (lm & 1);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(kb + swz(r, c), b0, b1, b2, b3);
+            mma_bf16(sc[0], qa0[kk], qa2[kk], b0, b1);
+            mma_bf16(sc[1], qa0[kk], qa2[kk], b2, b3);
+          }
+          float x[4];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int rr = trow + nt * 8 + qc2 + e;
+              const bool ok = qr < G && rr < nr && ((msk[rr] >> qr) & 1u);
+              x[nt * 2 + e] = ok ? sc[nt][e] * scale_log2 : -INFINITY;
+            }
+          }
+          float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+          const bool grow = tmax > m;
+          if (__any_sync(0xffffffffu, grow)) {
+            const float mn = grow ? tmax : m;
+            const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+            lsum *= corr;
+            const float ca = __shfl_sync(0xffffffffu, corr, (lane & 3) * 8);
+            const float cb = __shfl_sync(0xffffffffu, corr, (lane & 3) * 8 + 4);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              oT[i][0] *= ca;
+              oT[i][1] *= cb;
+              oT[i][2] *= ca;
+              oT[i][3] *= cb;
+            }
+            m = mn;
+          }
+          float p[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) p[i] = (x[i] == -INFINITY) ? 0.f : exp2f(x[i] - m);
+          lsum += (p[0] + p[1]) + (p[2] + p[3]);
+          const uint32_t ph0 = pack_bf16(p[0], p[1]), ph2 = pack_bf16(p[2], p[3]);
+          const uint32_t pl0 = pack_bf16(p[0] - bf16_round(p[0]), p[1] - bf16_round(p[1]));
+          const uint32_t pl2 = pack_bf16(p[2] - bf16_round(p[2]), p[3] - bf16_round(p[3]));
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            const int r = (lm >> 1) * 8 + lr, c = 2 * mt + (lm & 1);
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(vb + swz(r, c), a0, a1, a2, a3);
+            mma_bf16_full(oT[mt], a0, a1, a2, a3, ph0, ph2);
+            mma_bf16_full(oT[mt], a0, a1, a2, a3, pl0, pl2);
+          }
+        }
+        ++consumed;
+        __syncwarp();
+        // the item's last slot is kept as merge scratch until the merge is done
+        if (!(last_c && cc == nst - 1) && lane == 0) mbar_arrive(&sm.empty[slot]);
+      }
+      // this unit's row masks and queries are read: the buffer may be refilled
+      if (lane == 0) mbar_arrive(&sm.freed[buf]);
+      if (last_c) {
+        const int bg = it_c / splits, split = it_c - bg * splits;
+        const int b = bg / Hkv, g = bg - b * Hkv;
+        float* st_o = reinterpret_cast<float*>(sm.ring[slot]);  // [warps][G][128]
+        float* st_m = st_o + kPkWarps * G * kD;                  // [warps][G]
+        float* st_l = st_m + kPkWarps * G;
+        float ls = lsum;
+        ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+        named_sync(2, kPkThreads);  // every consumer warp is done reading the slot
+        {
+          const int h0 = qc2, h1 = qc2 + 1;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (h0 < G) {
+              st_o[(warp * G + h0) * kD + 16 * i + qr] = oT[i][0];
+              st_o[(warp * G + h0) * kD + 16 * i + qr + 8] = oT[i][2];
+            }
+            if (h1 < G) {
+              st_o[(warp * G + h1) * kD + 16 * i + qr] = oT[i][1];
+              st_o[(warp * G + h1) * kD + 16 * i + qr + 8] = oT[i][3];
+            }
+          }
+        }
+        if (qr < G && (lane & 3) == 0) {
+          st_m[warp * G + qr] = m;
+          st_l[warp * G + qr] = ls;
+        }
+        named_sync(2, kPkThreads);
+        const int d = tid;  // 128 consumer threads == 128 dims
+        for (int j = 0; j < G; ++j) {
+          float M = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kPkWarps; ++w) M = fmaxf(M, st_m[w * G + j]);
+          float L = 0.f, O = 0.f;
+          if (M != -INFINITY) {
+#pragma unroll
+            for (int w = 0; w < kPkWarps; ++w) {
+              const float mw = st_m[w * G + j];
+              if (mw != -INFINITY) {
+                const float c = exp2f(mw - M);
+                L = fmaf(st_l[w * G + j], c, L);
+                O = fmaf(st_o[(w * G + j) * kD + d], c, O);
+              }
+            }
+          }
+          float* dst = part + (((size_t)b * Hq + g * G + j) * splits + split) * kPartStride;
+          dst[2 + d] = O;
+          if (d == 0) {
+            dst[0] = M;
+            dst[1] = L;
+          }
+        }
+        named_sync(2, kPkThreads);  // scratch read by all before the slot is released
+        if (lane == 0) mbar_arrive(&sm.empty[slot]);
+      }
+    }
+  }
+  pdl_launch_dependents();
+}
+
 int g_pk_sms = 0;
 
 template <int G>
@@ -449,9 +839,9 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
                         cudaEvent_t ev_attend) {
   const int splits = (g.max_seq_len + kPkItemTok - 1) / kPkItemTok;
   const int n_items = splits * g.B * g.Hkv;
-  const size_t smem = sizeof(PkSmem<G>);
+  const size_t smem = sizeof(WsSmem<G>);
   static_assert(sizeof(float) * kPkWarps * G * (kD + 2) <= kPkStageBytes, "epilogue scratch fits a ring slot");
-  auto kern = attend_union_pk_kernel<G>;
+  auto kern = attend_union_ws_kernel<G>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (!g_pk_sms) {
@@ -462,7 +852,7 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::min(n_items, 2 * g_pk_sms));
-  cfg.blockDim = dim3(kPkThreads);
+  cfg.blockDim = dim3(kWsThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -471,9 +861,9 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint16_t*>(q),
-                            reinterpret_cast<const char*>(kv.k_pages), reinterpret_cast<const char*>(kv.v_pages),
-                            kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
-                            n_items, out, g.out_dtype, lse);
+                         reinterpret_cast<const char*>(kv.k_pages), reinterpret_cast<const char*>(kv.v_pages),
+                         kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
+                         n_items);
   if (e != cudaSuccess) return e;
   if (ev_attend) cudaEventRecord(ev_attend, st);
   return launch_merge_parts_pdl(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st);
