@@ -7,27 +7,28 @@
 // latency an SM needs >100 KB of copies in flight.  A CTA per 8192-token range
 // (k_rows_mma.cu) holds only ~600 rows at N = 128K, S = 50: its ring drains at
 // the end of every range and refills only after the next CTA's prologue.
-// Here two CTAs per SM each loop over work units and the issue cursor of the
-// ring runs ahead across unit boundaries, so copies stay in flight while a
-// unit ends (epilogue) and the next one starts.
+// Here two CTAs per SM, warp-specialised (attend_union_ws_kernel below), loop
+// over work units; the producers' issue cursor runs ahead across unit and item
+// boundaries, so copies stay in flight while a unit ends and the next starts.
 //
 // Work unit = up to kPkBatch consecutive union rows of one item, item = one
-// 8192-token range of one (b, g); items come from an atomic counter (zeroed by
-// sbs_sample_kernel).  At the start of each unit the CTA resolves the NEXT
-// unit (selection words -> ascending union rows -> K/V row index + head mask,
-// all 128 threads, page ids in registers) into the other half of a double
-// buffer; the issue cursor then streams the current unit's stages and, two
-// stages before its end, the next unit's.
+// 8192-token range of one (b, g); a CTA's first item is blockIdx.x, the rest
+// are claimed one item ahead from an atomic counter (zeroed by
+// sbs_sample_kernel).  The producers resolve the NEXT unit (selection words ->
+// ascending union rows -> K/V row index + head mask, page ids in registers)
+// into the other half of a double buffer while the consumers work on the
+// current one.
 //
-// Per 64-row stage each warp runs its 16-row tile on the tensor cores
+// Per 64-row stage each consumer warp runs its 16-row tile on the tensor cores
 // (mma.sync m16n8k16 bf16 -> fp32): S = Q K^T, masked online softmax,
 // O += (P_hi + P_lo) V; the arithmetic is that of attend_rows_mma_kernel.
-// At an item's last unit the 4 warps' states are merged (scratch: the ring
-// slot just consumed, which the cursor has not refilled yet) into the item's
-// split partial; merge_parts_kernel (PDL) merges the splits in split order
-// (deterministic) into out / lse.  Folding that merge into the last CTA of
-// each (b, g) needs a gpu-scope fence per item (MEMBAR.ALL.GPU + CCTL.IVALL),
-// which drains the ring's in-flight copies: measured 122 -> 240 us at cfg3.
+// At an item's last unit the 4 consumer warps' states are merged (scratch: the
+// ring slot just consumed, released to the producers only after the merge)
+// into the item's split partial; merge_parts_kernel (PDL) merges the splits in
+// split order (deterministic) into out / lse.  Folding that merge into the
+// last CTA of each (b, g) needs a gpu-scope fence per item (MEMBAR.ALL.GPU +
+// CCTL.IVALL), which drains the in-flight copies: measured 122 -> 240 us at
+// cfg3 (barrier-synchronised version).
 #include "sd_common.cuh"
 #include "sd_internal.h"
 #include "sd_sbs.cuh"
@@ -46,23 +47,9 @@ constexpr int kPkBatch = 1024;                            // union rows per work
 constexpr int kPkItemTok = kRangeTok;                     // 8192 tokens per item
 static_assert(kPkItemTok / 32 == 2 * kPkThreads, "two selection words per thread");
 
-template <int G>
-struct PkSmem {
-  unsigned char ring[kPkStages][kPkStageBytes];
-  uint32_t rowi[2][kPkBatch];  // K/V row index (page * 16 + slot) * Hkv + g
-  uint8_t rmask[2][kPkBatch];  // bit j: q-head j of the group selected the row
-  uint16_t qs[2][G * kD];      // the unit's item's queries
-  int wtot[kPkWarps];
-};
 
 __device__ __forceinline__ void cp_async16_pk(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_upto(int n) {  // at most n most recent groups pending
-  if (n <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-  else if (n == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-  else asm volatile("cp.async.wait_group 2;" ::: "memory");
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -103,344 +90,6 @@ __device__ __forceinline__ float bf16_round(float x) {
 }
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * kPkRowB + ((c ^ (r & 7)) << 4)); }
 
-template <int G>
-__global__ void __launch_bounds__(kPkThreads, 2) attend_union_pk_kernel(
-    const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
-    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int n_items,
-    void* __restrict__ out, int out_dtype, float* __restrict__ lse_out) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  PkSmem<G>& sm = *reinterpret_cast<PkSmem<G>*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int Hq = Hkv * G;
-
-  // ---- per-item inputs, prefetched into registers one item ahead: length,
-  // the 2 selection words per head and 4 page ids under them, the queries
-  struct ItemRegs {
-    int it, N;
-    uint2 wv[G];
-    int pv[4];
-    uint4 qv;
-  };
-  auto load_item = [&](ItemRegs& r, int it) {
-    r.it = it;
-    if (it >= n_items) return;
-    const int bg = it / splits, split = it - bg * splits;
-    const int b = bg / Hkv, g = bg - b * Hkv;
-    r.N = __ldg(seq_lens + b);
-    const int t0 = split * kPkItemTok;  // words / pages past N_b are masked at expansion
-    const int w0 = (t0 >> 5) + 2 * tid;  // even: 8-B aligned (ldw is even)
-#pragma unroll
-    for (int j = 0; j < G; ++j)
-      r.wv[j] = w0 < ldw ? *reinterpret_cast<const uint2*>(fbm + (size_t)(b * Hq + g * G + j) * ldw + w0)
-                         : make_uint2(0u, 0u);
-    const int p0 = (t0 >> 4) + 4 * tid;
-    const int* pt = page_table + (size_t)b * max_pages;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) r.pv[k] = p0 + k < max_pages ? __ldg(pt + p0 + k) : 0;
-    if (tid < G * 16) r.qv = *reinterpret_cast<const uint4*>(q + (size_t)(b * Hq + g * G + (tid >> 4)) * kD + (tid & 15) * 8);
-  };
-  // ---- rows [r0, r0 + kPkBatch) of the item in `r` -> buffer `buf`; returns
-  // the item's union row count.  All threads; 2 barriers.
-  auto resolve = [&](const ItemRegs& r, int r0, int buf) -> int {
-    const int it = r.it;
-    const int bg = it / splits, split = it - bg * splits;
-    const int g = bg - (bg / Hkv) * Hkv;
-    const int T0 = min(r.N, split * kPkItemTok), ntok = min(r.N, T0 + kPkItemTok) - T0;
-    const int nw = (ntok + 31) >> 5;
-    const int w0 = 2 * tid;
-    if (r0 == 0 && tid < G * 16) *reinterpret_cast<uint4*>(&sm.qs[buf][(tid >> 4) * kD + (tid & 15) * 8]) = r.qv;
-    uint32_t u0 = 0, u1 = 0;
-    uint2 wv[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      wv[j].x = w0 < nw ? r.wv[j].x : 0u;
-      wv[j].y = w0 + 1 < nw ? r.wv[j].y : 0u;
-      u0 |= wv[j].x;
-      u1 |= wv[j].y;
-    }
-    const int cnt = __popc(u0) + __popc(u1);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) sm.wtot[warp] = incl;
-    __syncthreads();
-    int pos = incl - cnt, total = 0;
-#pragma unroll
-    for (int w = 0; w < kPkWarps; ++w) {
-      const int t = sm.wtot[w];
-      pos += w < warp ? t : 0;
-      total += t;
-    }
-    if (pos < r0 + kPkBatch && pos + cnt > r0) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        uint32_t x = e ? u1 : u0;
-        while (x) {
-          const int bit = __ffs(x) - 1;
-          x &= x - 1;
-          if (pos >= r0 && pos < r0 + kPkBatch) {
-            uint32_t mk = 0;
-#pragma unroll
-            for (int j = 0; j < G; ++j) mk |= (((e ? wv[j].y : wv[j].x) >> bit) & 1u) << j;
-            const int pg = bit < 16 ? r.pv[2 * e] : r.pv[2 * e + 1];
-            sm.rowi[buf][pos - r0] = (uint32_t)(pg * kPS + (bit & 15)) * (uint32_t)Hkv + g;
-            sm.rmask[buf][pos - r0] = (uint8_t)mk;
-          }
-          ++pos;
-        }
-      }
-    }
-    __syncthreads();
-    return total;
-  };
-
-  // ---- static work assignment: items blockIdx.x, + gridDim.x, ...
-  int it_c = blockIdx.x;
-  if (it_c >= n_items) {
-    pdl_launch_dependents();
-    return;
-  }
-  ItemRegs cur_r, nxt_r;  // cur_r: the item being streamed; nxt_r: the next item (prefetched)
-  pdl_wait();  // selection bitmaps come from sbs_select_kernel
-  load_item(cur_r, it_c);
-  int r0_c = 0, buf_c = 0;
-  int total_c = resolve(cur_r, 0, 0);
-  load_item(nxt_r, it_c + gridDim.x);
-  int nrows_c = min(kPkBatch, total_c), nst_c = max(1, (nrows_c + kPkStageRows - 1) / kPkStageRows);
-  // issue cursor: ic_c stages of the current unit and ic_n of the next one issued
-  int ic_c = 0, ic_n = 0, cc = 0;  // cc: stages of the current unit computed
-  int issued = 0, computed = 0;     // global stage counters (ring slot = counter % kPkStages)
-
-  // cp.async issue mapping: thread copies 16-B chunk tid % 16 of rows tid / 16 + 8 i
-  const int ic16 = tid & 15, ir0 = tid >> 4;
-  const char* kpc = kp + ic16 * 16;
-  const char* vpc = vp + ic16 * 16;
-  auto issue = [&](int buf, int stage, int nrows) {
-    const uint32_t kd = smem_u32(&sm.ring[issued % kPkStages][0]);
-    const uint32_t vd = kd + kPkStageRows * kPkRowB;
-    const int R0 = stage * kPkStageRows;
-    const int nr = min(kPkStageRows, nrows - R0);
-    const int nr16 = (nr + 15) & ~15;  // rows of partial tiles are zero-filled
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = ir0 + 8 * i;
-      if (r < nr16) {
-        const bool valid = r < nr;
-        const size_t off = valid ? (size_t)sm.rowi[buf][R0 + r] * kPkRowB : 0;
-        const uint32_t d = (uint32_t)(r * kPkRowB + ((ic16 ^ (r & 7)) << 4));
-        cp_async16_pk(kd + d, kpc + off, valid);
-        cp_async16_pk(vd + d, vpc + off, valid);
-      }
-    }
-    cp_commit();
-    ++issued;
-  };
-
-  const int qr = lane >> 2, qc2 = (lane & 3) * 2;
-  const int lr = lane & 7, lm = lane >> 3;
-  uint32_t qa0[8], qa2[8];
-  // O^T accumulators: m-tile mt covers dims [16 mt, 16 mt + 16); lane (g, t)
-  // holds O[head 2t][dim g], O[head 2t+1][dim g], O[head 2t][dim g+8], O[head 2t+1][dim g+8]
-  float oT[8][4];
-  float m = -INFINITY, lsum = 0.f;
-
-  for (;;) {
-    // ---- unit start: (re)load state for a new item, resolve the next unit
-    if (r0_c == 0) {
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        qa0[kk] = qa2[kk] = 0u;
-        if (qr < G) {
-          const uint16_t* qrow = &sm.qs[buf_c][qr * kD + kk * 16 + qc2];
-          qa0[kk] = *reinterpret_cast<const uint32_t*>(qrow);
-          qa2[kk] = *reinterpret_cast<const uint32_t*>(qrow + 8);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
-      m = -INFINITY;
-      lsum = 0.f;
-    }
-    const bool last_c = r0_c + kPkBatch >= total_c;
-    int it_n, r0_n, total_n = 0, nrows_n = 0, nst_n = 0;
-    if (!last_c) {  // another batch of the same item (its words are still in cur_r)
-      it_n = it_c;
-      r0_n = r0_c + kPkBatch;
-      total_n = resolve(cur_r, r0_n, buf_c ^ 1);
-    } else {
-      it_n = nxt_r.it;
-      r0_n = 0;
-      if (it_n < n_items) {
-        total_n = resolve(nxt_r, 0, buf_c ^ 1);
-        cur_r = nxt_r;
-        load_item(nxt_r, it_n + gridDim.x);  // in flight while this unit streams
-      }
-    }
-    const bool has_n = it_n < n_items;
-    if (has_n) {
-      nrows_n = min(kPkBatch, total_n - r0_n);
-      nst_n = max(1, (nrows_n + kPkStageRows - 1) / kPkStageRows);
-    }
-    // ---- stream the current unit
-    for (; cc < nst_c; ++cc) {
-      // top up: keep the current stage + 2 more issued
-      while (issued < computed + kPkStages) {
-        if (ic_c < nst_c) {
-          issue(buf_c, ic_c++, nrows_c);
-        } else if (ic_n < nst_n) {
-          issue(buf_c ^ 1, ic_n++, nrows_n);
-        } else {
-          break;
-        }
-      }
-      cp_wait_upto(issued - computed - 1);
-      __syncthreads();
-      const unsigned char* st = sm.ring[computed % kPkStages];
-      const uint8_t* msk = sm.rmask[buf_c] + cc * kPkStageRows;
-      const int nr = min(kPkStageRows, nrows_c - cc * kPkStageRows);
-      const int trow = warp * kPkTile;
-      if (trow < nr) {
-        const uint32_t kb = smem_u32(st) + trow * kPkRowB;
-        const uint32_t vb = smem_u32(st + kPkStageRows * kPkRowB) + trow * kPkRowB;
-        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const int r = (lm >> 1) * 8 + lr, c = 2 * kk + (lm & 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(kb + swz(r, c), b0, b1, b2, b3);
-          mma_bf16(sc[0], qa0[kk], qa2[kk], b0, b1);
-          mma_bf16(sc[1], qa0[kk], qa2[kk], b2, b3);
-        }
-        float x[4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int rr = trow + nt * 8 + qc2 + e;
-            const bool ok = qr < G && rr < nr && ((msk[rr] >> qr) & 1u);
-            x[nt * 2 + e] = ok ? sc[nt][e] * scale_log2 : -INFINITY;
-          }
-        }
-        float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-        const bool grow = tmax > m;
-        if (__any_sync(0xffffffffu, grow)) {
-          const float mn = grow ? tmax : m;
-          const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mn);
-          lsum *= corr;
-          // this lane's O^T columns are heads 2t, 2t+1: their factors live in lanes 8t, 8t + 4
-          const float ca = __shfl_sync(0xffffffffu, corr, (lane & 3) * 8);
-          const float cb = __shfl_sync(0xffffffffu, corr, (lane & 3) * 8 + 4);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            oT[i][0] *= ca;
-            oT[i][1] *= cb;
-            oT[i][2] *= ca;
-            oT[i][3] *= cb;
-          }
-          m = mn;
-        }
-        float p[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) p[i] = (x[i] == -INFINITY) ? 0.f : exp2f(x[i] - m);
-        lsum += (p[0] + p[1]) + (p[2] + p[3]);
-        const uint32_t ph0 = pack_bf16(p[0], p[1]), ph2 = pack_bf16(p[2], p[3]);
-        const uint32_t pl0 = pack_bf16(p[0] - bf16_round(p[0]), p[1] - bf16_round(p[1]));
-        const uint32_t pl2 = pack_bf16(p[2] - bf16_round(p[2]), p[3] - bf16_round(p[3]));
-        // O^T += V^T P^T: A = V^T tile (16 dims x 16 tokens, ldmatrix.trans of
-        // the token-major rows), B = P^T = the S fragments of this lane as they are
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          const int r = (lm >> 1) * 8 + lr, c = 2 * mt + (lm & 1);
-          uint32_t a0, a1, a2, a3;
-          ldsm_x4_t(vb + swz(r, c), a0, a1, a2, a3);
-          mma_bf16_full(oT[mt], a0, a1, a2, a3, ph0, ph2);
-          mma_bf16_full(oT[mt], a0, a1, a2, a3, pl0, pl2);
-        }
-      }
-      ++computed;
-      __syncthreads();  // the slot may be refilled by the next top-up
-    }
-    // ---- item end: merge the 4 warps' states into the item's split partial.
-    // Scratch: the slot of the stage just computed (not refilled before the
-    // next top-up).
-    if (last_c) {
-      const int bg = it_c / splits, split = it_c - bg * splits;
-      const int b = bg / Hkv, g = bg - b * Hkv;
-      float* st_o = reinterpret_cast<float*>(sm.ring[(computed + kPkStages - 1) % kPkStages]);  // [warps][G][128]
-      float* st_m = st_o + kPkWarps * G * kD;                                                     // [warps][G]
-      float* st_l = st_m + kPkWarps * G;
-      float ls = lsum;
-      ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-      ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-      {
-        const int h0 = qc2, h1 = qc2 + 1;  // this lane's two heads (2t, 2t+1)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (h0 < G) {
-            st_o[(warp * G + h0) * kD + 16 * i + qr] = oT[i][0];
-            st_o[(warp * G + h0) * kD + 16 * i + qr + 8] = oT[i][2];
-          }
-          if (h1 < G) {
-            st_o[(warp * G + h1) * kD + 16 * i + qr] = oT[i][1];
-            st_o[(warp * G + h1) * kD + 16 * i + qr + 8] = oT[i][3];
-          }
-        }
-      }
-      if (qr < G) {
-        if ((lane & 3) == 0) {
-          st_m[warp * G + qr] = m;
-          st_l[warp * G + qr] = ls;
-        }
-      }
-      __syncthreads();
-      const int d = tid;  // 128 threads == 128 dims
-      for (int j = 0; j < G; ++j) {
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < kPkWarps; ++w) M = fmaxf(M, st_m[w * G + j]);
-        float L = 0.f, O = 0.f;
-        if (M != -INFINITY) {
-#pragma unroll
-          for (int w = 0; w < kPkWarps; ++w) {
-            const float mw = st_m[w * G + j];
-            if (mw != -INFINITY) {
-              const float c = exp2f(mw - M);
-              L = fmaf(st_l[w * G + j], c, L);
-              O = fmaf(st_o[(w * G + j) * kD + d], c, O);
-            }
-          }
-        }
-        float* dst = part + (((size_t)b * Hq + g * G + j) * splits + split) * kPartStride;
-        dst[2 + d] = O;
-        if (d == 0) {
-          dst[0] = M;
-          dst[1] = L;
-        }
-      }
-      __syncthreads();  // scratch slot free before the next top-up
-    }
-    if (!has_n) break;
-    // ---- advance: the next unit becomes current (its issued stages carry over)
-    it_c = it_n;
-    r0_c = r0_n;
-    buf_c ^= 1;
-    total_c = total_n;
-    nrows_c = nrows_n;
-    nst_c = nst_n;
-    ic_c = ic_n;
-    ic_n = 0;
-    cc = 0;
-  }
-  cp_wait_upto(0);
-  pdl_launch_dependents();
-}
-
 // ---------------------------------------------------------------------------
 // Warp-specialised variant (default): 8 warps per CTA, 2 CTAs per SM.
 // Warps 4-7 (producers, 56 registers after setmaxnreg.dec) resolve work units
@@ -463,6 +112,7 @@ struct WsSmem {
   uint16_t qs[2][G * kD];
   int u_it[2], u_nrows[2], u_last[2], u_r0[2];
   int wtot[kPkWarps];
+  int next_it;  // dynamically claimed next item (producers)
   uint64_t full[kPkStages], empty[kPkStages], ready[2], freed[2];
 };
 
@@ -475,7 +125,8 @@ template <int G>
 __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
     const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
     const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int n_items) {
+    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int n_items,
+    int* __restrict__ work) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   WsSmem<G>& sm = *reinterpret_cast<WsSmem<G>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -623,11 +274,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
       ++issued;
     };
 
+    // items: blockIdx.x first, then claimed from the work counter (zeroed by
+    // sbs_sample_kernel) one item ahead, so faster CTAs take more items
+    auto claim = [&]() {
+      if (pt_ == 0) sm.next_it = gridDim.x + atomicAdd(work, 1);
+      named_sync(1, kPkThreads);
+      return sm.next_it;
+    };
     ItemRegs cur_r, nxt_r;
     int it_c = blockIdx.x, r0_c = 0;
     load_item(cur_r, it_c);
     int total_c = resolve(cur_r, 0, 0);
-    load_item(nxt_r, it_c + gridDim.x);
+    load_item(nxt_r, claim());
     int u = 0;
     int nrows_c = min(kPkBatch, total_c);
     publish(0, it_c, 0, nrows_c, r0_c + kPkBatch >= total_c);
@@ -656,7 +314,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
       } else {
         total_n = resolve(nxt_r, 0, nb);
         cur_r = nxt_r;
-        load_item(nxt_r, it_n + gridDim.x);
+        load_item(nxt_r, claim());
       }
       const int nrows_n = min(kPkBatch, total_n - r0_n);
       publish(u + 1, it_n, r0_n, nrows_n, r0_n + kPkBatch >= total_n);
@@ -863,7 +521,7 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
   e = cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint16_t*>(q),
                          reinterpret_cast<const char*>(kv.k_pages), reinterpret_cast<const char*>(kv.v_pages),
                          kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
-                         n_items);
+                         n_items, counters + g.B * g.Hkv);
   if (e != cudaSuccess) return e;
   if (ev_attend) cudaEventRecord(ev_attend, st);
   return launch_merge_parts_pdl(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st);
