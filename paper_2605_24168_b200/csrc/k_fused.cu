@@ -80,12 +80,19 @@ __device__ __forceinline__ int hidx(uint32_t b) { return (int)(b + (b >> 6)); }
 // Warp-level search of a padded 2048-bin histogram (highest bin = largest
 // keys) for the bin holding the r-th largest element; returns (bin, residual
 // rank).  Two parallel levels: 32 groups of 64 bins, then 32 pairs of bins.
-__device__ __forceinline__ void warp_find_bin(const uint32_t* hist, uint32_t r, int* bin_out, uint32_t* res_out) {
+// With `grp` (the 32 group sums, grp[k] = bins [64 k, 64 k + 63]) the first
+// level is one load per lane instead of 64.
+__device__ __forceinline__ void warp_find_bin(const uint32_t* hist, uint32_t r, int* bin_out, uint32_t* res_out,
+                                              const uint32_t* grp = nullptr) {
   const int lane = threadIdx.x & 31;
   const int top = 2047 - 64 * lane;  // lane owns bins [top - 63, top]
   uint32_t sum = 0;
+  if (grp) {
+    sum = grp[31 - lane];
+  } else {
 #pragma unroll 16
-  for (int i = 0; i < 64; ++i) sum += hist[hidx(top - i)];
+    for (int i = 0; i < 64; ++i) sum += hist[hidx(top - i)];
+  }
   uint32_t incl = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -117,6 +124,28 @@ __device__ __forceinline__ void warp_find_bin(const uint32_t* hist, uint32_t r, 
   }
   *bin_out = __shfl_sync(0xffffffffu, bin, src2);
   *res_out = __shfl_sync(0xffffffffu, res, src2);
+}
+
+// Group sums of nh padded 2048-bin histograms: grp[h][k] = sum of bins
+// [64 k, 64 k + 63] of histogram h (8 threads per group, shuffle reduction).
+// All NT threads call it; NT % 32 == 0.
+template <int NT>
+__device__ __forceinline__ void hist_group_sums(const uint32_t* hist, int nh, uint32_t* grp) {
+  for (int base = 0; base < nh * 32 * 8; base += NT) {
+    const int i = base + threadIdx.x;  // 8 consecutive threads per group
+    const int gi = i >> 3, part = i & 7;
+    uint32_t v = 0;
+    if (gi < nh * 32) {
+      const uint32_t* h = hist + (gi >> 5) * kHistWords;
+      const int b0 = (gi & 31) * 64 + part * 8;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v += h[hidx(b0 + k)];
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (part == 0 && gi < nh * 32) grp[gi] = v;
+  }
 }
 
 // two independent fp32 fma's in one FFMA2 (bit-identical to two fmaf)
@@ -203,17 +232,25 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   uint32_t* hist1 = reinterpret_cast<uint32_t*>(smem);  // [G][kHistWords] padded 2048-bin
   uint32_t* hist2 = hist1 + G * kHistWords;              // [G][2][256]
   float* qc = reinterpret_cast<float*>(hist2 + G * 512);  // [G][C]
+  unsigned char* s_qrow = reinterpret_cast<unsigned char*>(qc + G * C);  // [G][kD] q dtype (fp32 at most)
+  int* s_ch = reinterpret_cast<int*>(s_qrow + (size_t)G * kD * 4);        // [C]
+  uint32_t* s_grp = reinterpret_cast<uint32_t*>(s_ch + C);               // [G][32] level-1 group sums
   __shared__ int s_bin1[G][2];
   __shared__ uint32_t s_res[G][2];
   __shared__ uint32_t s_lohi[G][2];
   const int bg = blockIdx.x, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the channel ids and the group's whole q rows are requested first (no
+  // dependence), then the sample's sketch rows (N -> page ids -> rows is the
+  // longest dependent chain); the histogram clearing and the barrier overlap
+  const int qb = q_dtype == SD_F32 ? 4 : 2;
+  const int chv = tid < C ? __ldg(channel_ids + (size_t)bg * C + tid) : 0;
+  const int nq16 = G * kD * qb / 16;
+  const uint4* qsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)(b * Hq + g * G) * kD * qb);
+  const uint4 qv = tid < nq16 ? __ldg(qsrc + tid) : make_uint4(0u, 0u, 0u, 0u);
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
-  // the sample's sketch rows first (N -> page ids -> rows is the longest
-  // dependent chain); the q channels, the histogram clearing and the barrier
-  // overlap with those loads
   const int npg = (max(N, 1) + 15) >> 4;
   const int cap_pages = CAP >> 4;
   const int spg = (npg + cap_pages - 1) / cap_pages;  // page stride
@@ -228,12 +265,18 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     tt[u] = (i < n_slots && t < N) ? t : -1;
     if (tt[u] >= 0) raw[u] = Sk::load8(sk, sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
-  load_qc<G>(qc, q, q_dtype, channel_ids, b, g, Hkv, C, kSampleThreads);
   for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist1[i] = 0;
   for (int i = tid; i < G * 512; i += kSampleThreads) hist2[i] = 0;
+  if (tid < C) s_ch[tid] = chv;
+  if (tid < nq16) reinterpret_cast<uint4*>(s_qrow)[tid] = qv;
   if (tid == 0) {
     counters[bg] = 0;                   // re-arm the gather-attend merge counter of (b, g)
     if (bg == 0) counters[gridDim.x] = 0;  // and the work counter
+  }
+  __syncthreads();
+  for (int i = tid; i < G * C; i += kSampleThreads) {  // qc[j][c] = q[b][g G + j][channel_ids[b][g][c]]
+    const int j = i / C, e = j * kD + s_ch[i - j * C];
+    qc[i] = qb == 4 ? reinterpret_cast<const float*>(s_qrow)[e] : bf_lo(reinterpret_cast<const uint16_t*>(s_qrow)[e]);
   }
   __syncthreads();
   if (N < 1) return;
@@ -276,12 +319,14 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   }
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
   __syncthreads();
+  hist_group_sums<kSampleThreads>(hist1, G, s_grp);
+  __syncthreads();
   // level 1: warp 2 j + e finds the 11-bit bin of rank (ra, rb)[e] for head j
   if (warp < 2 * G) {
     const int j = warp >> 1, e = warp & 1;
     int bin;
     uint32_t res;
-    warp_find_bin(hist1 + j * kHistWords, e ? rb : ra, &bin, &res);
+    warp_find_bin(hist1 + j * kHistWords, e ? rb : ra, &bin, &res, s_grp + j * 32);
     if (lane == 0) {
       s_bin1[j][e] = bin;
       s_res[j][e] = res;
@@ -1093,7 +1138,8 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int BG = geo.B * geo.Hkv;
   cudaError_t e;
   {
-    const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C;
+    const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C + (size_t)G * kD * 4 +
+                        sizeof(int) * C + sizeof(uint32_t) * G * 32;
     auto kern = sbs_sample_kernel<G, Sk>;
     set_smem(kern, smem);
     e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
