@@ -461,7 +461,7 @@ def main():
     if os.path.exists(tp):
         tj = json.load(open(tp)).get(args.config if world == 1 else f"{args.config}_tp{world}")
         if tj:
-            traffic = tj.get("kernels", {}).get("attend_union_pk_kernel")
+            traffic = tj.get("kernels", {}).get("attend_union_ws_kernel")
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -474,7 +474,7 @@ def main():
         "hbm_gbs": step_achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "peak_source": src,
-                     "kernel": "attend_union_pk_kernel (GQA-union gather-attend)",
+                     "kernel": "attend_union_ws_kernel (GQA-union gather-attend)",
                      "algorithmic_bytes_per_launch": attend_bytes, "launch_us": phases_us["attend"],
                      "share_of_step": phases_us["attend"] / serial_us},
         "step_roofline": {"achieved": step_achieved, "frac": step_achieved / hbm,

@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["sbs_sample_kernel", "sbs_scan_kernel", "sbs_select_kernel", "attend_union_pk_kernel",
+KERNELS = ["sbs_sample_kernel", "sbs_scan_kernel", "sbs_select_kernel", "attend_union_ws_kernel",
            "merge_parts_kernel"]
 WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Executed Ipc Active", "Issue Slots Busy",
         "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy", "Waves Per SM", "L2 Hit Rate"]
