@@ -667,37 +667,47 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
       auto phase1 = [&](auto np_tag, auto full_tag) {
         constexpr int NP = decltype(np_tag)::value;
         constexpr bool FULL = decltype(full_tag)::value;
-#pragma unroll 4
-        for (int i0 = 0; i0 < kScanStageTok8; i0 += kScanNT) {
-          if (wn > kCap - kPerBlk) flush();
-          const int blk = i0 + warp * 32;
-          uint32_t a[4];
-          sk_mma_a_smem(a, smem_u32(st + (size_t)blk * 16));
-          float d[4] = {0.f, 0.f, 0.f, 0.f};
-          sk_mma(d, a, qm.b[0]);  // the accumulation order of sk_mma_score
-          if constexpr (NP > 1) {
-            sk_mma(d, a, qm.b[1]);
-            sk_mma(d, a, qm.b[2]);
-          }
-          const int tA = blk + pm_r + ((pm_u >> 1) << 4), tB = tA + 8;
-          if constexpr (!FULL) {
-            if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
-              if (tbase + tA < rb.lo || tbase + tA >= rb.hi) d[0] = d[1] = INFINITY;
-              if (tbase + tB < rb.lo || tbase + tB >= rb.hi) d[2] = d[3] = INFINITY;
+        // two 32-token blocks per flush check: both fragments and MMAs are
+        // issued before either block's compares (no control dependence between them)
+        constexpr int kB = 2;
+#pragma unroll 2
+        for (int i0 = 0; i0 < kScanStageTok8; i0 += kB * kScanNT) {
+          if (wn > kCap - kB * kPerBlk) flush();
+          float d[kB][4];
+#pragma unroll
+          for (int h = 0; h < kB; ++h) {
+            uint32_t a[4];
+            sk_mma_a_smem(a, smem_u32(st + (size_t)(i0 + h * kScanNT + warp * 32) * 16));
+            d[h][0] = d[h][1] = d[h][2] = d[h][3] = 0.f;
+            sk_mma(d[h], a, qm.b[0]);  // the accumulation order of sk_mma_score
+            if constexpr (NP > 1) {
+              sk_mma(d[h], a, qm.b[1]);
+              sk_mma(d[h], a, qm.b[2]);
             }
           }
-          bool cA = d[0] >= pm_fl0 || d[1] >= pm_fl1;
-          bool cB = d[2] >= pm_fl0 || d[3] >= pm_fl1;
-          if constexpr (!FULL) {
-            cA = cA && tA < lim;
-            cB = cB && tB < lim;
+#pragma unroll
+          for (int h = 0; h < kB; ++h) {
+            const int blk = i0 + h * kScanNT + warp * 32;
+            const int tA = blk + pm_r + ((pm_u >> 1) << 4), tB = tA + 8;
+            if constexpr (!FULL) {
+              if (edge_stage) {  // NEXT-1: sink / local tokens rank above every score
+                if (tbase + tA < rb.lo || tbase + tA >= rb.hi) d[h][0] = d[h][1] = INFINITY;
+                if (tbase + tB < rb.lo || tbase + tB >= rb.hi) d[h][2] = d[h][3] = INFINITY;
+              }
+            }
+            bool cA = d[h][0] >= pm_fl0 || d[h][1] >= pm_fl1;
+            bool cB = d[h][2] >= pm_fl0 || d[h][3] >= pm_fl1;
+            if constexpr (!FULL) {
+              cA = cA && tA < lim;
+              cB = cB && tB < lim;
+            }
+            const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
+            const int nA = __popc(bA);
+            const int pA = wn + __popc(bA & lt_mask), pB = wn + nA + __popc(bB & lt_mask);
+            st_cand_pred(cA, pm_c2 + pA, d[h][0], d[h][1], pm_ct + pA, (uint16_t)((cb + tA) | (pm_p << 15)));
+            st_cand_pred(cB, pm_c2 + pB, d[h][2], d[h][3], pm_ct + pB, (uint16_t)((cb + tB) | (pm_p << 15)));
+            wn += nA + __popc(bB);
           }
-          const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
-          const int nA = __popc(bA);
-          const int pA = wn + __popc(bA & lt_mask), pB = wn + nA + __popc(bB & lt_mask);
-          st_cand_pred(cA, pm_c2 + pA, d[0], d[1], pm_ct + pA, (uint16_t)((cb + tA) | (pm_p << 15)));
-          st_cand_pred(cB, pm_c2 + pB, d[2], d[3], pm_ct + pB, (uint16_t)((cb + tB) | (pm_p << 15)));
-          wn += nA + __popc(bB);
         }
       };
       const bool full = lim == kScanStageTok8 && !edge_stage;
