@@ -60,16 +60,6 @@ __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t 
                            : bf_lo(reinterpret_cast<const uint16_t*>(q)[e]);
 }
 
-// qc[j][c] = q[b][g*G + j][channel_ids[b][g][c]]
-template <int G>
-__device__ __forceinline__ void load_qc(float* qc, const void* q, int q_dtype, const int* channel_ids, int b,
-                                        int g, int Hkv, int C, int nthreads) {
-  const int Hq = Hkv * G;
-  for (int i = threadIdx.x; i < G * C; i += nthreads) {
-    const int j = i / C, c = i - j * C;
-    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
-    qc[i] = load_q_elem(q, q_dtype, ((size_t)b * Hq + g * G + j) * kD + ch);
-  }
 }
 
 // 2048-bin histograms are stored padded, bin b at hidx(b) = b + b / 64, so
