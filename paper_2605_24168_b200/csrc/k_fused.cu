@@ -60,8 +60,6 @@ __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t 
                            : bf_lo(reinterpret_cast<const uint16_t*>(q)[e]);
 }
 
-}
-
 // 2048-bin histograms are stored padded, bin b at hidx(b) = b + b / 64, so
 // that a warp reading 64-bin groups (one group per lane) is bank-conflict-free.
 constexpr int kHistWords = 2048 + 32;
