@@ -147,6 +147,14 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, 
   a1 = __uint_as_float((uint32_t)(r >> 32));
 }
 
+// Global stores with an L2 cache-policy hint (evict-last: data re-read soon).
+__device__ __forceinline__ void st_keep_u32(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep_f2(float2* p, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+
 // Predicated candidate store (no branch): {x, y} -> *c2, code -> *ct when p.
 __device__ __forceinline__ void st_cand_pred(bool p, float2* c2, float x, float y, uint16_t* ct, uint16_t code) {
   asm volatile(
@@ -558,6 +566,10 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     fsure[j] = th.y == 0xFFFFFFFFu ? INFINITY : thresh_lo(th.y + 1u);  // key > hi  <=>  s >= fsure
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
+  // band entries and selection words are read by the select right after this
+  // kernel: keep them in L2 ahead of the streamed sketch (evict-last stores)
+  uint64_t pol_keep;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
   uint32_t* rtok = ent_tok + reg * CW;
   float* rsc = ent_sc + reg * CW * G;
   float* c_sc = c_sc_all + warp * G * kScanCandCap;  // this warp's candidates ([p][G])
@@ -596,8 +608,8 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
           const int pos = (p ? wc1 : wc) + __popc((p ? b1 : b0) & lt_mask);
           if (pos < CW) {
             const size_t e = (reg * 2 + p) * CW + pos;
-            ent_tok[e] = (uint32_t)(t0 + i) | (m << 24);
-            reinterpret_cast<float2*>(ent_sc)[e] = v;
+            st_keep_u32(ent_tok + e, (uint32_t)(t0 + i) | (m << 24), pol_keep);
+            st_keep_f2(reinterpret_cast<float2*>(ent_sc) + e, v, pol_keep);
           }
         }
         wc += __popc(b0);
@@ -763,7 +775,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int nwv = (ntok + 31) >> 5;
   for (int i = tid; i < G * kWords; i += kScanNT) {
     const int j = i / kWords, w = i - j * kWords;
-    if (w < nwv) fbm[(size_t)(row0 + j) * ldw + (t0 >> 5) + w] = s_words[i];
+    if (w < nwv) st_keep_u32(fbm + (size_t)(row0 + j) * ldw + (t0 >> 5) + w, s_words[i], pol_keep);
   }
   if (kMma) {
     if (lane == 0) {
