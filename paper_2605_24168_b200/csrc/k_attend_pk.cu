@@ -475,10 +475,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
             }
           }
           float* dst = part + (((size_t)b * Hq + g * G + j) * splits + split) * kPartStride;
-          dst[2 + d] = O;
+          const uint64_t pol = l2_policy_evict_last();  // re-read by merge_parts_kernel
+          st_keep_f32(dst + 2 + d, O, pol);
           if (d == 0) {
-            dst[0] = M;
-            dst[1] = L;
+            st_keep_f32(dst, M, pol);
+            st_keep_f32(dst + 1, L, pol);
           }
         }
         named_sync(2, kPkThreads);  // scratch read by all before the slot is released

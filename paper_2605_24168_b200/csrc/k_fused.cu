@@ -147,14 +147,6 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, 
   a1 = __uint_as_float((uint32_t)(r >> 32));
 }
 
-// Global stores with an L2 cache-policy hint (evict-last: data re-read soon).
-__device__ __forceinline__ void st_keep_u32(uint32_t* p, uint32_t v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_keep_f2(float2* p, float2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
-}
-
 // Predicated candidate store (no branch): {x, y} -> *c2, code -> *ct when p.
 __device__ __forceinline__ void st_cand_pred(bool p, float2* c2, float x, float y, uint16_t* ct, uint16_t code) {
   asm volatile(
@@ -568,8 +560,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const uint32_t lt_mask = (1u << lane) - 1u;
   // band entries and selection words are read by the select right after this
   // kernel: keep them in L2 ahead of the streamed sketch (evict-last stores)
-  uint64_t pol_keep;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+  const uint64_t pol_keep = l2_policy_evict_last();
   uint32_t* rtok = ent_tok + reg * CW;
   float* rsc = ent_sc + reg * CW * G;
   float* c_sc = c_sc_all + warp * G * kScanCandCap;  // this warp's candidates ([p][G])
