@@ -582,3 +582,25 @@ def test_fused_fast_path_taken(cuda_lib, dist, lens):
     sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE)
     assert sd.read_stats()["fallback_rows"] == 0
     assert sd.read_device_error() == 0
+
+
+@pytest.mark.parametrize("S,N", [(50.0, 40000), (2.0, 131072)])
+def test_fused_g4_pair_select_and_ws_attend(cuda_lib, S, N):
+    """G = 4 (the tensor-core scan's head-pair regions): at S = 50 the select runs
+    one CTA per head pair (two 256-thread halves); at S = 2, N = 128K its band
+    capacity exceeds two heads per CTA and one CTA per head reads the pair
+    regions.  Both feed the warp-specialised attend (dynamic item claiming):
+    parity on rows of both heads of every pair, no slow path, and two calls
+    bitwise identical."""
+    sd = cuda_lib
+    case = workloads.make_case(1, 32, 8, [N], seed=97, dist="needle", n_needles=30)
+    rows = [(0, h) for h in (0, 1, 2, 3, 14, 15, 30, 31)]
+    _check_fused(sd, case, S, "sketch", rows=rows)
+    dc = _dev(case)
+    kv, sk = _kv(sd, dc)
+    sd.clear_device_error()
+    a = sd.sparse_decode_fused(dc.q, kv, sk, S=S, scale=SCALE, out_dtype=torch.float32, return_idx=True)
+    assert sd.read_stats()["fallback_rows"] == 0
+    b = sd.sparse_decode_fused(dc.q, kv, sk, S=S, scale=SCALE, out_dtype=torch.float32, return_idx=True)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
