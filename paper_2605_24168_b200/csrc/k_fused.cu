@@ -356,8 +356,10 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     if (r_lo > n_s) lo = 0u;         // not enough sample mass: every token is a candidate
     if (r_hi < 1) hi = 0xFFFFFFFFu;  // no token is sure
     const size_t row = (size_t)b * Hq + g * G + tid;
-    thr[row * 2 + 0] = lo;
-    thr[row * 2 + 1] = hi;
+    // keys for the select; the equivalent float thresholds for the scan
+    // (score >= flo <=> key >= lo;  score >= fsure <=> key > hi)
+    const float flo = thresh_lo(lo), fsure = hi == 0xFFFFFFFFu ? INFINITY : thresh_lo(hi + 1u);
+    reinterpret_cast<uint4*>(thr)[row] = make_uint4(lo, hi, __float_as_uint(flo), __float_as_uint(fsure));
   }
   pdl_launch_dependents();
 }
@@ -462,9 +464,9 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     if (tid + u * kScanNT < nq16) qv[u] = __ldg(qsrc + tid + u * kScanNT);
   for (int i = tid; i < G * kWords; i += kScanNT) s_words[i] = 0u;
   pdl_wait();  // the bracket comes from the sample kernel
-  uint2 thv[G];
+  float2 thv[G];  // {flo, fsure} per head, converted by the sample kernel
 #pragma unroll
-  for (int j = 0; j < G; ++j) thv[j] = __ldg(reinterpret_cast<const uint2*>(thr) + row0 + j);
+  for (int j = 0; j < G; ++j) thv[j] = __ldg(reinterpret_cast<const float2*>(thr) + 2 * (row0 + j) + 1);
   if (t0 >= N) {
     if (kMma) {
       if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
@@ -553,9 +555,8 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   float flo[G], fsure[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    const uint2 th = thv[j];
-    flo[j] = thresh_lo(th.x);
-    fsure[j] = th.y == 0xFFFFFFFFu ? INFINITY : thresh_lo(th.y + 1u);  // key > hi  <=>  s >= fsure
+    flo[j] = thv[j].x;
+    fsure[j] = thv[j].y;  // key > hi  <=>  s >= fsure
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
   // band entries and selection words are read by the select right after this
@@ -849,7 +850,7 @@ __global__ void __launch_bounds__(Two ? 2 * kSelNT : kSelNT, Two ? 2 : 4) sbs_se
   }
   const int row = row_base + h;  // this half's row
   uint32_t* fr = fbm + (size_t)row * ldw;
-  const uint32_t lo = thr[row * 2 + 0], hi = thr[row * 2 + 1];
+  const uint32_t lo = thr[row * 4 + 0], hi = thr[row * 4 + 1];
   const int nw = (N + 31) >> 5;
   __syncthreads();
   // ---- sure count: the scan's bits of the half's row

@@ -34,8 +34,8 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
     off = align256(off + rows * (size_t)k_max * sizeof(int));
     L.counts = off;
     off = align256(off + rows * sizeof(int));
-    L.thr = off;
-    off = align256(off + rows * 2 * sizeof(uint32_t));
+    L.thr = off;  // {lo key, hi key, flo, fsure} per row
+    off = align256(off + rows * 4 * sizeof(uint32_t));
     const int G = Hq / Hkv;
     const size_t nreg = (size_t)B * Hkv * L.nrange * kScanWarps;
     const size_t cap = band_region_cap(G);

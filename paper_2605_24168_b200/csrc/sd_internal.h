@@ -46,7 +46,7 @@ struct WsLayout {
   int k_max = 0;
   // fused path (sample-bracket select, sd_sbs.cuh)
   int nrange = 0, ldw = 0;
-  size_t thr = 0;            // uint32 [B*Hq][2]
+  size_t thr = 0;            // uint32 [B*Hq][4]: bracket keys lo, hi; float thresholds flo, fsure
   size_t ent_tok = 0;        // uint32 token | head mask << 24  [B*Hkv][nrange * 8][cap]  (union band)
   size_t ent_sc = 0;         // float scores [B*Hkv][nrange * 8][cap][G]
   size_t ent_cnt = 0;        // int32 [B*Hkv][nrange * 8] entry counts (> cap: overflow)

@@ -3,7 +3,8 @@
 // (k_rows_mma.cu, k_rows.cu).
 //
 // Per q-row (b, h) with N_b tokens:
-//   thr[row] = {lo, hi}      sample bracket keys                       (sbs_sample_kernel)
+//   thr[row] = {lo, hi, flo, fsure}  sample bracket keys + the equivalent fp32
+//                                    thresholds for the scan        (sbs_sample_kernel)
 //   fbm[row][t / 32] bit t = key(s_t) > hi after sbs_scan_kernel (sure tokens),
 //                          = t is in the exact top-k_b after sbs_select_kernel
 //   band entries (lo <= key <= hi for some head of the group): per (b, g,

@@ -87,6 +87,10 @@ __device__ __forceinline__ SkMmaQ sk_mma_q(QF qf, int np) {
   r.np = np;
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
+    if (p >= np) {  // bf16 q: one exact part
+      r.b[p][0] = r.b[p][1] = 0u;
+      continue;
+    }
     const uint16_t h0 = sk_to_bf16(v0), h1 = sk_to_bf16(v1);
     const uint32_t w = (uint32_t)h0 | ((uint32_t)h1 << 16);
     r.b[p][0] = grp == 0 ? w : 0u;
