@@ -442,7 +442,7 @@ def test_fused_equals_unfused_chain(cuda_lib):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["cfg2_s10", "cfg2_s100", "cfg3"])
+@pytest.mark.parametrize("name", ["cfg2_s10", "cfg2_s100", "cfg3", "cfg4_t33", "cfg4_t66"])
 def test_fused_baseline_sizes_sampled_rows(cuda_lib, name):
     """BASELINE.json full sizes in the bench's launch configuration; the oracle
     checks sampled (b, h) rows one by one."""
