@@ -45,8 +45,23 @@ namespace sd {
 namespace {
 
 constexpr float kBracketZ = 4.0f;
-constexpr int kSampleThreads = 1024;
-constexpr int kSampleSlots = 4;            // sample tokens per thread (cap 4096)
+constexpr int kSampleThreads = 1024;      // sample CTA (one per (b, g)): 4096-token sample, 1 CTA/SM
+constexpr int kSampleSlots = 4;            // sample tokens per thread
+// More (b, g) rows than SMs and sequences up to 80K tokens: 512-thread CTAs
+// (2048-token sample, 2 CTAs/SM), one wave instead of two.  Longer sequences
+// keep the 4096-token sample: the bracket (and the select's band) widens as
+// sqrt(k N / sample) and costs more than the second sample wave (cfg4 turn 66:
+// 376 vs 389 us).
+static int sample_threads(int rows_bg, int max_seq_len) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return rows_bg > sms && max_seq_len <= 81920 ? 512 : kSampleThreads;
+}
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
@@ -210,12 +225,12 @@ __device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, 
   *res_out = __shfl_sync(0xffffffffu, res, src);
 }
 
-template <int G, class Sk>
-__global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
+template <int G, class Sk, int NT>
+__global__ void __launch_bounds__(NT) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
     BudgetDev bud, uint32_t* __restrict__ thr, int* __restrict__ counters) {
-  constexpr int CAP = kSampleThreads * kSampleSlots;
+  constexpr int CAP = NT * kSampleSlots;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* hist1 = reinterpret_cast<uint32_t*>(smem);  // [G][kHistWords] padded 2048-bin
   uint32_t* hist2 = hist1 + G * kHistWords;              // [G][2][256]
@@ -248,13 +263,13 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   int tt[kSampleSlots];
 #pragma unroll
   for (int u = 0; u < kSampleSlots; ++u) {
-    const int i = tid + u * kSampleThreads;
+    const int i = tid + u * NT;
     const int t = (i >> 4) * spg * 16 + (i & 15);
     tt[u] = (i < n_slots && t < N) ? t : -1;
     if (tt[u] >= 0) raw[u] = Sk::load8(sk, sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
   }
-  for (int i = tid; i < G * kHistWords; i += kSampleThreads) hist1[i] = 0;
-  for (int i = tid; i < G * 512; i += kSampleThreads) hist2[i] = 0;
+  for (int i = tid; i < G * kHistWords; i += NT) hist1[i] = 0;
+  for (int i = tid; i < G * 512; i += NT) hist2[i] = 0;
   if (tid < C) s_ch[tid] = chv;
   if (tid < nq16) reinterpret_cast<uint4*>(s_qrow)[tid] = qv;
   if (tid == 0) {
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
     if (bg == 0) counters[gridDim.x] = 0;  // and the work counter
   }
   __syncthreads();
-  for (int i = tid; i < G * C; i += kSampleThreads) {  // qc[j][c] = q[b][g G + j][channel_ids[b][g][c]]
+  for (int i = tid; i < G * C; i += NT) {  // qc[j][c] = q[b][g G + j][channel_ids[b][g][c]]
     const int j = i / C, e = j * kD + s_ch[i - j * C];
     qc[i] = qb == 4 ? reinterpret_cast<const float*>(s_qrow)[e] : bf_lo(reinterpret_cast<const uint16_t*>(s_qrow)[e]);
   }
@@ -307,7 +322,7 @@ __global__ void __launch_bounds__(kSampleThreads) sbs_sample_kernel(
   }
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
   __syncthreads();
-  hist_group_sums<kSampleThreads>(hist1, G, s_grp);
+  hist_group_sums<NT>(hist1, G, s_grp);
   __syncthreads();
   // level 1: warp 2 j + e finds the 11-bit bin of rank (ra, rb)[e] for head j
   if (warp < 2 * G) {
@@ -1166,12 +1181,12 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 // (sigma = sqrt(k f (1 - f)), f = sample fraction) plus the two edge bins;
 // sized at 1.25x that + 1024, within [4096, kSelCap] (4 select CTAs per SM at
 // the low end, 1 at the high end).
-int band_capacity(int max_seq_len, Budget bud) {
+int band_capacity(int max_seq_len, Budget bud, int sample_nt) {
   const double N = std::max(1, max_seq_len);
   const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N)
                    : bud.regions() ? std::max(1.0, bud.heavy_fraction * N + bud.n_sink + bud.n_local)
                                    : std::ceil(N / bud.S);
-  const double f = std::min(1.0, (double)(kSampleThreads * kSampleSlots) / N);
+  const double f = std::min(1.0, (double)(sample_nt * kSampleSlots) / N);
   const double sig = std::sqrt(k * f * (1.0 - f));
   const double band = (2.0 * kBracketZ * sig + 2.0) / f;
   const int cap = (int)std::min<double>(kSelCap, std::max(4096.0, 1.25 * band + 1024.0));
@@ -1188,9 +1203,10 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   {
     const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C + (size_t)G * kD * 4 +
                         sizeof(int) * C + sizeof(uint32_t) * G * 32;
-    auto kern = sbs_sample_kernel<G, Sk>;
+    const int snt = sample_threads(BG, geo.max_seq_len);
+    auto kern = snt == 512 ? sbs_sample_kernel<G, Sk, 512> : sbs_sample_kernel<G, Sk, kSampleThreads>;
     set_smem(kern, smem);
-    e = launch_pdl(kern, dim3(BG), dim3(kSampleThreads), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
+    e = launch_pdl(kern, dim3(BG), dim3(snt), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[0], st);
@@ -1212,7 +1228,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
   {
-    const int sel_cap = band_capacity(geo.max_seq_len, bud);
+    const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len));
     const bool pair = SkMma<G, Sk>::value && C == 8;
     const size_t smem1 = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
     // two heads per CTA when that still fits 2 CTAs per SM (B*Hq/2 pairs in one wave)
