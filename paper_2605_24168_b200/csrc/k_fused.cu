@@ -52,7 +52,7 @@ constexpr int kSampleSlots = 4;            // sample tokens per thread
 // keep the 4096-token sample: the bracket (and the select's band) widens as
 // sqrt(k N / sample) and costs more than the second sample wave (cfg4 turn 66:
 // 376 vs 389 us).
-static int sample_threads(int rows_bg, int max_seq_len) {
+static int sm_count() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -60,7 +60,10 @@ static int sample_threads(int rows_bg, int max_seq_len) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  return rows_bg > sms && max_seq_len <= 81920 ? 512 : kSampleThreads;
+  return sms;
+}
+static int sample_threads(int rows_bg, int max_seq_len) {
+  return rows_bg > sm_count() && max_seq_len <= 81920 ? 512 : kSampleThreads;
 }
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
@@ -225,7 +228,9 @@ __device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, 
   *res_out = __shfl_sync(0xffffffffu, res, src);
 }
 
-template <int G, class Sk, int NT>
+// GG = the GQA group size, G = the heads one CTA handles (GG / G CTAs per (b, g)
+// share the group's sample rows when there are few (b, g) rows).
+template <int GG, class Sk, int NT, int G>
 __global__ void __launch_bounds__(NT) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
@@ -241,8 +246,10 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   __shared__ int s_bin1[G][2];
   __shared__ uint32_t s_res[G][2];
   __shared__ uint32_t s_lohi[G][2];
-  const int bg = blockIdx.x, b = bg / Hkv, g = bg - b * Hkv;
-  const int Hq = Hkv * G;
+  constexpr int kParts = GG / G;
+  const int part = blockIdx.x % kParts, bg = blockIdx.x / kParts, b = bg / Hkv, g = bg - b * Hkv;
+  const int j0 = part * G;  // this CTA's heads: j0 .. j0 + G - 1 of the group
+  const int Hq = Hkv * GG;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // the channel ids and the group's whole q rows are requested first (no
   // dependence), then the sample's sketch rows (N -> page ids -> rows is the
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   const int qb = q_dtype == SD_F32 ? 4 : 2;
   const int chv = tid < C ? __ldg(channel_ids + (size_t)bg * C + tid) : 0;
   const int nq16 = G * kD * qb / 16;
-  const uint4* qsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)(b * Hq + g * G) * kD * qb);
+  const uint4* qsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)(b * Hq + g * GG + j0) * kD * qb);
   const uint4 qv = tid < nq16 ? __ldg(qsrc + tid) : make_uint4(0u, 0u, 0u, 0u);
   const int N = __ldg(seq_lens + b);
   const int* pt = page_table + (size_t)b * max_pages;
@@ -273,8 +280,8 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   if (tid < C) s_ch[tid] = chv;
   if (tid < nq16) reinterpret_cast<uint4*>(s_qrow)[tid] = qv;
   if (tid == 0) {
-    counters[bg] = 0;                   // re-arm the gather-attend merge counter of (b, g)
-    if (bg == 0) counters[gridDim.x] = 0;  // and the work counter
+    if (part == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
+    if (blockIdx.x == 0) counters[gridDim.x / kParts] = 0;  // and the work counter
   }
   __syncthreads();
   for (int i = tid; i < G * C; i += NT) {  // qc[j][c] = q[b][g G + j][channel_ids[b][g][c]]
@@ -370,7 +377,7 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
     uint32_t lo = s_lohi[tid][0], hi = s_lohi[tid][1];
     if (r_lo > n_s) lo = 0u;         // not enough sample mass: every token is a candidate
     if (r_hi < 1) hi = 0xFFFFFFFFu;  // no token is sure
-    const size_t row = (size_t)b * Hq + g * G + tid;
+    const size_t row = (size_t)b * Hq + g * GG + j0 + tid;
     // keys for the select; the equivalent float thresholds for the scan
     // (score >= flo <=> key >= lo;  score >= fsure <=> key > hi)
     const float flo = thresh_lo(lo), fsure = hi == 0xFFFFFFFFu ? INFINITY : thresh_lo(hi + 1u);
@@ -1204,9 +1211,16 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C + (size_t)G * kD * 4 +
                         sizeof(int) * C + sizeof(uint32_t) * G * 32;
     const int snt = sample_threads(BG, geo.max_seq_len);
-    auto kern = snt == 512 ? sbs_sample_kernel<G, Sk, 512> : sbs_sample_kernel<G, Sk, kSampleThreads>;
-    set_smem(kern, smem);
-    e = launch_pdl(kern, dim3(BG), dim3(snt), smem, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
+    // few (b, g) rows: two CTAs per (b, g), half the heads each (fills more SMs)
+    constexpr int GH = G >= 2 ? G / 2 : 1;
+    const bool split = G >= 2 && snt == kSampleThreads && 2 * BG <= sm_count();
+    auto kern = snt == 512 ? sbs_sample_kernel<G, Sk, 512, G>
+                           : split ? sbs_sample_kernel<G, Sk, kSampleThreads, GH> : sbs_sample_kernel<G, Sk, kSampleThreads, G>;
+    const size_t smem_used = split ? sizeof(uint32_t) * GH * (kHistWords + 512) + sizeof(float) * GH * C + (size_t)GH * kD * 4 +
+                                         sizeof(int) * C + sizeof(uint32_t) * GH * 32
+                                   : smem;
+    set_smem(kern, smem_used);
+    e = launch_pdl(kern, dim3(split ? 2 * BG : BG), dim3(snt), smem_used, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
                    kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[0], st);
