@@ -88,7 +88,11 @@ typedef struct {
  *                      at (page_table[b][t / page_size], t % page_size)
  *   seq_lens         : int32 [B], 1 <= N_b <= max_seq_len (device)
  *   max_seq_len      : HOST-side upper bound on every N_b (sizes grids and the
- *                      workspace without reading device memory).                */
+ *                      workspace without reading device memory).  Every kernel
+ *                      reads N_b against it: a row with N_b < 1 or
+ *                      N_b > max_seq_len is treated as empty (nothing is read
+ *                      or written for it; out = 0, lse = -inf) and the device
+ *                      error word is set to SD_DEVERR_SEQLEN.                   */
 typedef struct {
   const void* k_pages;
   const void* v_pages;
@@ -119,7 +123,9 @@ typedef struct {
 /* Sparsity budget ("each query-head attends to 1/S fraction of total
  * tokens").  k_b = max(1, ceil(N_b / sparsity)) evaluated in double
  * precision, or k_fixed when k_fixed > 0 (absolute form; k_fixed > N_b
- * is a device error SD_DEVERR_SEQLEN).
+ * is a device error SD_DEVERR_SEQLEN).  Both fractional fields are doubles, so
+ * a budget such as S = 1.3 or heavy_fraction = 0.7 means exactly what the
+ * SPEC's double arithmetic gives.
  * Sink + Local + heavy (NEXT-1), active when any of
  * n_sink, n_local, heavy_fraction is non-zero: with lo = min(n_sink, N_b),
  * hi = max(lo, N_b - min(n_local, N_b)), mid = hi - lo, the row keeps every
@@ -129,11 +135,11 @@ typedef struct {
  * rows.  n_sink, n_local >= 0 and 0 <= heavy_fraction <= 1, else INVALID_ARG;
  * the sequence-shard entries return UNSUPPORTED for such budgets. */
 typedef struct {
-  float sparsity;
+  double sparsity;
   int32_t k_fixed;
   int32_t n_sink;
   int32_t n_local;
-  float heavy_fraction;
+  double heavy_fraction;
 } sd_budget;
 
 /* ---- host helpers --------------------------------------------------------- */
@@ -242,6 +248,19 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
                                  int32_t k_max_out, void* ws, size_t ws_bytes,
                                  sd_stream stream);
 
+/* sd_sparse_decode_fused with option flags (0 = sd_sparse_decode_fused):
+ *   SD_FUSED_FORCE_SLOW_PATH - every row of the sketch-mode selection takes the
+ *   exact slow path (all scores recomputed, full radix select): the result is
+ *   identical by construction, which the tests check.  Any other bit:
+ *   SD_ERR_INVALID_ARG. */
+enum { SD_FUSED_FORCE_SLOW_PATH = 1 };
+sd_status sd_sparse_decode_fused_ex(const sd_geometry* geom, const sd_paged_kv* kv,
+                                    const sd_sketch* sketch, const void* q,
+                                    const sd_budget* budget, float scale, void* out,
+                                    float* lse, int32_t* idx_out, int32_t* counts_out,
+                                    int32_t k_max_out, void* ws, size_t ws_bytes,
+                                    uint32_t flags, sd_stream stream);
+
 /* Measurement helper (not for production use): sd_sparse_decode_fused in
  * sketch mode with a CUDA event recorded after each of its kernels; it
  * synchronizes `stream` and writes the kernels' durations in milliseconds to
@@ -283,7 +302,9 @@ sd_status sd_lse_merge(int32_t parts, int32_t rows, int32_t D, const float* part
  *     (ties: lower rank first, then lower local position - equal to lower
  *     global index) fixes how many of this rank's candidates survive; attend
  *     over them -> normalised part_o fp32 [B][Hq][D], part_lse fp32 [B][Hq]
- *     (-inf when none survive).
+ *     (-inf when none survive).  surv_idx (int32 [B][Hq][k_max], nullable)
+ *     receives the surviving LOCAL indices in increasing order and surv_counts
+ *     (int32 [B][Hq], nullable) their number (may be 0).
  * (4) all-gather partials, sd_lse_merge in rank order. */
 sd_status sd_seqshard_local_topk(const sd_geometry* geom, const sd_paged_kv* kv,
                                  const sd_sketch* sketch, const void* q,
@@ -299,6 +320,7 @@ sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv,
                                  const float* all_cand, const int32_t* cand_idx,
                                  int32_t k_max, int32_t parts, int32_t rank,
                                  float scale, float* part_o, float* part_lse,
+                                 int32_t* surv_idx, int32_t* surv_counts,
                                  void* ws, size_t ws_bytes, sd_stream stream);
 
 #ifdef __cplusplus

@@ -28,7 +28,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 __all__ = [
-    "budget_k", "token_location", "OracleInputs", "from_case", "index_scores",
+    "budget_k", "OracleInputs", "from_case", "index_scores",
     "topk_select", "attend", "dense_decode", "sparse_decode", "attend_given",
     "lse_merge", "seqshard_decode", "sink_local_heavy_select", "heavy_budget",
     "stochastic_select", "SparseResult",
@@ -78,13 +78,6 @@ def budget_k(S: float, N: int, k_fixed: int = 0) -> int:
     else:
         k = math.ceil(N / S)
     return max(1, int(k))
-
-
-# ---------------------------------------------------------------------------
-# A4 addressing: token t -> (page_ids[t // page_size], t mod page_size)
-# ---------------------------------------------------------------------------
-def token_location(page_table_row: Sequence[int], t: int, page_size: int):
-    return int(page_table_row[t // page_size]), int(t % page_size)
 
 
 @dataclass

@@ -22,6 +22,7 @@ SD_ERR_DEVICE_CHECK = 5
 SD_BF16 = 0
 SD_F32 = 1
 SD_E4M3 = 2  # fp8 e4m3 (sketch pages only, NEXT-4)
+SD_FUSED_FORCE_SLOW_PATH = 1  # sd_sparse_decode_fused_ex flag
 
 DEVERR = {0: "none", 1: "index out of range", 2: "indices not strictly increasing", 3: "empty index list",
           4: "weight <= 0 or non-finite", 5: "bad sequence length / budget", 6: "candidate overflow"}
@@ -48,8 +49,8 @@ class Sketch(ctypes.Structure):
 
 
 class Budget(ctypes.Structure):
-    _fields_ = [("sparsity", c_f32), ("k_fixed", c_i32), ("n_sink", c_i32), ("n_local", c_i32),
-                ("heavy_fraction", c_f32)]
+    _fields_ = [("sparsity", ctypes.c_double), ("k_fixed", c_i32), ("n_sink", c_i32), ("n_local", c_i32),
+                ("heavy_fraction", ctypes.c_double)]
 
 
 P = ctypes.POINTER
@@ -71,6 +72,8 @@ _PROTOS = {
                                         c_vp, c_vp, c_size, c_vp]),
     "sd_sparse_decode_fused": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_f32, c_vp, c_vp,
                                        c_vp, c_vp, c_i32, c_vp, c_size, c_vp]),
+    "sd_sparse_decode_fused_ex": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_f32, c_vp, c_vp,
+                                          c_vp, c_vp, c_i32, c_vp, c_size, ctypes.c_uint32, c_vp]),
     "sd_sparse_decode_fused_timed": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_f32, c_vp,
                                              c_vp, c_vp, c_size, c_vp, P(c_f32), c_i32]),
     "sd_dense_decode": (c_i32, [P(Geometry), P(PagedKV), c_vp, c_f32, c_vp, c_vp, c_vp, c_size, c_vp]),
@@ -78,7 +81,7 @@ _PROTOS = {
     "sd_seqshard_local_topk": (c_i32, [P(Geometry), P(PagedKV), P(Sketch), c_vp, P(Budget), c_vp, c_i32, c_vp,
                                        c_vp, c_i32, c_vp, c_size, c_vp]),
     "sd_seqshard_cut_attend": (c_i32, [P(Geometry), P(PagedKV), c_vp, P(Budget), c_vp, c_vp, c_vp, c_i32,
-                                       c_i32, c_i32, c_f32, c_vp, c_vp, c_vp, c_size, c_vp]),
+                                       c_i32, c_i32, c_f32, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

@@ -125,13 +125,18 @@ def workspace_size(geom: C.Geometry, budget: Optional[C.Budget], max_seq_len: in
 
 def workspace(nbytes: int, device=None, stream=None) -> torch.Tensor:
     """A zeroed (error word cleared) device workspace, cached per (device, stream)
-    and grown on demand."""
+    and grown on demand.  The buffer is allocated on (and recorded with) the
+    stream the library enqueues on, so the caching allocator never hands a
+    replaced buffer out while that stream may still use it."""
     device = torch.device(device or "cuda")
     s = stream if stream is not None else torch.cuda.current_stream(device)
     key = (device.index if device.index is not None else torch.cuda.current_device(), s.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
+        if ws is not None:
+            ws.record_stream(s)  # the old buffer stays reserved until s passes this point
+        with torch.cuda.stream(s):
+            ws = torch.zeros(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws
 
@@ -248,9 +253,11 @@ def sparse_gather_attend(q, kv: KVCache, idx, counts, weights=None, scale: Optio
 def sparse_decode_fused(q, kv: KVCache, sketch: Optional[SketchCache], S: float = 50.0, k_fixed: int = 0,
                         scale: Optional[float] = None, out_dtype=None, return_idx: bool = False, out=None,
                         lse=None, idx=None, counts=None, stream=None, n_sink: int = 0, n_local: int = 0,
-                        heavy_fraction: float = 0.0):
+                        heavy_fraction: float = 0.0, force_slow_path: bool = False):
     """A6: the fused decode step -> (out, lse) or (out, lse, idx, counts).  With
-    n_sink / n_local / heavy_fraction: the Sink + Local + heavy budget (NEXT-1)."""
+    n_sink / n_local / heavy_fraction: the Sink + Local + heavy budget (NEXT-1).
+    force_slow_path: every row on the exact slow selection path (sd_sparse_decode_fused_ex
+    SD_FUSED_FORCE_SLOW_PATH; same result, for tests)."""
     g = geometry(q, kv, out_dtype)
     bud = make_budget(S, k_fixed, n_sink, n_local, heavy_fraction)
     scale = scale if scale is not None else 1.0 / math.sqrt(q.shape[-1])
@@ -264,10 +271,14 @@ def sparse_decode_fused(q, kv: KVCache, sketch: Optional[SketchCache], S: float 
     sk = sketch.c_struct() if sketch is not None else None
     ws = workspace(workspace_size(g, bud, kv.max_seq_len), q.device, stream)
     p, n = _ws_ptr(ws)
-    _check(C.load().sd_sparse_decode_fused(ctypes.byref(g), ctypes.byref(kvs), ctypes.byref(sk) if sk else None,
-                                           _ptr(q), ctypes.byref(bud), float(scale), _ptr(out), _ptr(lse),
-                                           _ptr(idx), _ptr(counts), int(idx.shape[-1]) if idx is not None else 0,
-                                           p, n, _stream(stream)), "sd_sparse_decode_fused")
+    args = (ctypes.byref(g), ctypes.byref(kvs), ctypes.byref(sk) if sk else None, _ptr(q), ctypes.byref(bud),
+            float(scale), _ptr(out), _ptr(lse), _ptr(idx), _ptr(counts), int(idx.shape[-1]) if idx is not None else 0,
+            p, n)
+    if force_slow_path:
+        _check(C.load().sd_sparse_decode_fused_ex(*args, C.SD_FUSED_FORCE_SLOW_PATH, _stream(stream)),
+               "sd_sparse_decode_fused_ex")
+    else:
+        _check(C.load().sd_sparse_decode_fused(*args, _stream(stream)), "sd_sparse_decode_fused")
     if return_idx:
         return out, lse, idx, counts
     return out, lse
@@ -343,8 +354,9 @@ def seqshard_local_topk(q, kv: KVCache, sketch: Optional[SketchCache], global_se
 
 
 def seqshard_cut_attend(q, kv: KVCache, global_seq_lens, all_cand, cand_idx, rank: int, S: float,
-                        k_fixed: int = 0, scale: Optional[float] = None, stream=None):
-    """Sequence shard step (3): this rank's normalised partial (part_o fp32 [B][Hq][D], part_lse fp32 [B][Hq])."""
+                        k_fixed: int = 0, scale: Optional[float] = None, stream=None, return_survivors: bool = False):
+    """Sequence shard step (3): this rank's normalised partial (part_o fp32 [B][Hq][D], part_lse fp32 [B][Hq]),
+    plus (surv_idx int32 [B][Hq][k_max] LOCAL ascending, surv_counts int32 [B][Hq]) with return_survivors."""
     g = geometry(q, kv)
     bud = make_budget(S, k_fixed)
     P = all_cand.shape[0]
@@ -352,13 +364,19 @@ def seqshard_cut_attend(q, kv: KVCache, global_seq_lens, all_cand, cand_idx, ran
     scale = scale if scale is not None else 1.0 / math.sqrt(q.shape[-1])
     part_o = torch.empty(q.shape, dtype=torch.float32, device=q.device)
     part_lse = torch.empty(q.shape[:2], dtype=torch.float32, device=q.device)
+    surv = cnt = None
+    if return_survivors:
+        surv = torch.full((g.batch, g.num_q_heads, k_max), -1, dtype=torch.int32, device=q.device)
+        cnt = torch.zeros((g.batch, g.num_q_heads), dtype=torch.int32, device=q.device)
     kvs = kv.c_struct()
     ws = workspace(_ws_bytes_budget(g, bud, kv.max_seq_len, k_max), q.device, stream)
     p, n = _ws_ptr(ws)
     _check(C.load().sd_seqshard_cut_attend(ctypes.byref(g), ctypes.byref(kvs), _ptr(q), ctypes.byref(bud),
                                            _ptr(global_seq_lens), _ptr(all_cand), _ptr(cand_idx), int(k_max),
-                                           int(P), int(rank), float(scale), _ptr(part_o), _ptr(part_lse), p, n,
-                                           _stream(stream)), "sd_seqshard_cut_attend")
+                                           int(P), int(rank), float(scale), _ptr(part_o), _ptr(part_lse),
+                                           _ptr(surv), _ptr(cnt), p, n, _stream(stream)), "sd_seqshard_cut_attend")
+    if return_survivors:
+        return part_o, part_lse, surv, cnt
     return part_o, part_lse
 
 

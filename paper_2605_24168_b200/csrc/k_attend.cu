@@ -56,7 +56,7 @@ __device__ __forceinline__ void cta_combine_store(float (*st_o)[kD], float* st_m
 template <class KV>
 __global__ void __launch_bounds__(kAttThreads) attend_list_kernel(
     const void* __restrict__ q, const void* __restrict__ kp, const void* __restrict__ vp,
-    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages,
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages,
     int Hq, int Hkv, const int* __restrict__ idx, const int* __restrict__ counts, int k_max,
     const float* __restrict__ weights, float scale_log2, float* __restrict__ part, int splits,
     int allow_empty, int* __restrict__ err) {
@@ -65,11 +65,11 @@ __global__ void __launch_bounds__(kAttThreads) attend_list_kernel(
 
   const int row = blockIdx.y, split = blockIdx.x;
   const int b = row / Hq, h = row - b * Hq, g = h / (Hq / Hkv);
-  const int N = __ldg(seq_lens + b);
+  const int N = seq_len_dev(seq_lens, b, max_len);  // -1 (out of range): every count is rejected
   int cnt = __ldg(counts + row);
   if ((cnt < 1 && !allow_empty) || cnt > k_max || cnt > N) {
     if (split == 0 && threadIdx.x == 0) set_error(err, cnt < 1 ? SD_DEVERR_EMPTY : SD_DEVERR_SEQLEN);
-    cnt = max(0, min(cnt, min(k_max, N)));
+    cnt = max(0, min(cnt, min(k_max, max(N, 0))));
   }
   const int per = (cnt + splits - 1) / splits;
   const int c0 = min(cnt, split * per), c1 = min(cnt, c0 + per);
@@ -150,90 +150,6 @@ __global__ void __launch_bounds__(kAttThreads) attend_list_kernel(
   if (l16 == 0) { st_m[hw] = m; st_l[hw] = l; }
   __syncthreads();
   cta_combine_store(st_o, st_m, st_l, part + ((size_t)row * splits + split) * kPartStride);
-}
-
-// ---------------------------------------------------------------------------
-// Dense decode: all N_b rows; each K/V row is loaded once and used
-// by the G q-heads of its KV head.  grid = (splits, B*Hkv); block = 128.
-// ---------------------------------------------------------------------------
-template <class KV, int G>
-__global__ void __launch_bounds__(kAttThreads) dense_kernel(
-    const void* __restrict__ q, const void* __restrict__ kp, const void* __restrict__ vp,
-    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages,
-    int Hkv, float scale_log2, float* __restrict__ part, int splits) {
-  __shared__ float st_o[G][kHalfWarps][kD];
-  __shared__ float st_m[G][kHalfWarps], st_l[G][kHalfWarps];
-
-  const int bg = blockIdx.y, split = blockIdx.x;
-  const int b = bg / Hkv, g = bg - b * Hkv;
-  const int Hq = Hkv * G;
-  const int N = __ldg(seq_lens + b);
-  const int per = (((N + splits - 1) / splits) + 15) & ~15;
-  const int t0 = min(N, split * per), t1 = min(N, t0 + per);
-
-  const int lane = threadIdx.x & 31, l16 = lane & 15, hw = threadIdx.x >> 4;
-  float qf[G][8];
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    load_q8<KV>(q, ((size_t)b * Hq + g * G + j) * kD + l16 * 8, qf[j]);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) qf[j][e] *= scale_log2;
-  }
-  const int* pt = page_table + (size_t)b * max_pages;
-  float m[G], l[G], o[G][8];
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    m[j] = -INFINITY; l[j] = 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) o[j][e] = 0.f;
-  }
-  for (int it = t0; it < t1; it += kHalfWarps * kUnroll) {
-    typename KV::Raw kr[kUnroll], vr[kUnroll];
-    bool ok[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      int t = it + u * kHalfWarps + hw;
-      ok[u] = t < t1;
-      if (!ok[u]) t = t0;
-      const size_t re = kv_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv) + l16 * 8;
-      kr[u] = KV::load(kp, re);
-      vr[u] = KV::load(vp, re);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      float kf[8], vf[8];
-      KV::unpack(kr[u], kf);
-      KV::unpack(vr[u], vf);
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        float s = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s = fmaf(qf[j][e], kf[e], s);
-        s = half_warp_sum(s);
-        if (ok[u]) {
-          const float mn = fmaxf(m[j], s);
-          const float corr = exp2f(m[j] - mn);
-          const float p = exp2f(s - mn);
-          l[j] = fmaf(l[j], corr, p);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) o[j][e] = fmaf(o[j][e], corr, p * vf[e]);
-          m[j] = mn;
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) st_o[j][hw][l16 * 8 + e] = o[j][e];
-    if (l16 == 0) { st_m[j][hw] = m[j]; st_l[j][hw] = l[j]; }
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int j = 0; j < G; ++j) {
-    const int row = b * Hq + g * G + j;
-    cta_combine_store(st_o[j], st_m[j], st_l[j], part + ((size_t)row * splits + split) * kPartStride);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -355,36 +271,12 @@ cudaError_t launch_attend_list(const Geo& g, const sd_paged_kv& kv, const void* 
   const float sl2 = scale * kLog2e;
   if (g.kv_dtype == SD_BF16)
     attend_list_kernel<KvBF16><<<grid, kAttThreads, 0, st>>>(
-        q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens, g.max_pages, g.Hq, g.Hkv, idx,
+        q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hq, g.Hkv, idx,
         counts, k_max, weights, sl2, part, splits, allow_empty, err);
   else
     attend_list_kernel<KvF32><<<grid, kAttThreads, 0, st>>>(
-        q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens, g.max_pages, g.Hq, g.Hkv, idx,
+        q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hq, g.Hkv, idx,
         counts, k_max, weights, sl2, part, splits, allow_empty, err);
-  return cudaGetLastError();
-}
-
-template <class KV>
-static void dense_dispatch(const Geo& g, const sd_paged_kv& kv, const void* q, float sl2,
-                           float* part, int splits, cudaStream_t st) {
-  dim3 grid(splits, g.B * g.Hkv);
-#define SD_DENSE(GG)                                                                         \
-  dense_kernel<KV, GG><<<grid, kAttThreads, 0, st>>>(q, kv.k_pages, kv.v_pages, kv.page_table, \
-                                                     kv.seq_lens, g.max_pages, g.Hkv, sl2, part, splits)
-  switch (g.G) {
-    case 1: SD_DENSE(1); break;
-    case 2: SD_DENSE(2); break;
-    case 4: SD_DENSE(4); break;
-    case 8: SD_DENSE(8); break;
-  }
-#undef SD_DENSE
-}
-
-cudaError_t launch_dense(const Geo& g, const sd_paged_kv& kv, const void* q, float scale,
-                         float* part, int splits, cudaStream_t st) {
-  const float sl2 = scale * kLog2e;
-  if (g.kv_dtype == SD_BF16) dense_dispatch<KvBF16>(g, kv, q, sl2, part, splits, st);
-  else dense_dispatch<KvF32>(g, kv, q, sl2, part, splits, st);
   return cudaGetLastError();
 }
 

@@ -124,7 +124,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 template <int G>
 __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
     const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
-    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int n_items,
     int* __restrict__ work) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
       if (it >= n_items) return;
       const int bg = it / splits, split = it - bg * splits;
       const int b = bg / Hkv, g = bg - b * Hkv;
-      r.N = __ldg(seq_lens + b);
+      r.N = max(0, seq_len_dev(seq_lens, b, max_len));  // out of range: an empty row (the select reports)
       const int t0 = split * kPkItemTok;
       const int w0 = (t0 >> 5) + 2 * pt_;
 #pragma unroll
@@ -490,8 +490,6 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
   pdl_launch_dependents();
 }
 
-int g_pk_sms = 0;
-
 template <int G>
 cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
                         float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st,
@@ -501,16 +499,10 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
   const size_t smem = sizeof(WsSmem<G>);
   static_assert(sizeof(float) * kPkWarps * G * (kD + 2) <= kPkStageBytes, "epilogue scratch fits a ring slot");
   auto kern = attend_union_ws_kernel<G>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  if (!g_pk_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_pk_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_pk_sms <= 0) g_pk_sms = 148;
-  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::min(n_items, 2 * g_pk_sms));
+  cfg.gridDim = dim3(std::min(n_items, 2 * g.sms));
   cfg.blockDim = dim3(kWsThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -521,7 +513,7 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint16_t*>(q),
                          reinterpret_cast<const char*>(kv.k_pages), reinterpret_cast<const char*>(kv.v_pages),
-                         kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
+                         kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
                          n_items, counters + g.B * g.Hkv);
   if (e != cudaSuccess) return e;
   if (ev_attend) cudaEventRecord(ev_attend, st);

@@ -52,18 +52,8 @@ constexpr int kSampleSlots = 4;            // sample tokens per thread
 // keep the 4096-token sample: the bracket (and the select's band) widens as
 // sqrt(k N / sample) and costs more than the second sample wave (cfg4 turn 66:
 // 376 vs 389 us).
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-static int sample_threads(int rows_bg, int max_seq_len) {
-  return rows_bg > sm_count() && max_seq_len <= 81920 ? 512 : kSampleThreads;
+static int sample_threads(int rows_bg, int max_seq_len, int sms) {
+  return rows_bg > sms && max_seq_len <= 81920 ? 512 : kSampleThreads;
 }
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
@@ -233,7 +223,7 @@ __device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, 
 template <int GG, class Sk, int NT, int G>
 __global__ void __launch_bounds__(NT) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     BudgetDev bud, uint32_t* __restrict__ thr, int* __restrict__ counters) {
   constexpr int CAP = NT * kSampleSlots;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -259,7 +249,7 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   const int nq16 = G * kD * qb / 16;
   const uint4* qsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)(b * Hq + g * GG + j0) * kD * qb);
   const uint4 qv = tid < nq16 ? __ldg(qsrc + tid) : make_uint4(0u, 0u, 0u, 0u);
-  const int N = __ldg(seq_lens + b);
+  const int N = seq_len_dev(seq_lens, b, max_len);  // < 1: an empty row (the select reports it)
   const int* pt = page_table + (size_t)b * max_pages;
   const int npg = (max(N, 1) + 15) >> 4;
   const int cap_pages = CAP >> 4;
@@ -434,7 +424,7 @@ __device__ __forceinline__ void load_scores(float (&sc)[G], const float* src) {
 template <int G, bool C8, class Sk>
 __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
     int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud) {
   constexpr int NW = kScanNT / 32;
@@ -470,7 +460,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   // brackets once the sample kernel has finished), so the CTA start costs one
   // memory round trip instead of four
   const int qb = q_dtype == SD_F32 ? 4 : 2;
-  const int N = __ldg(seq_lens + b);
+  const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // out of range: an empty row
   const int* pt = page_table + (size_t)b * max_pages + (t0 >> 4);
   const int np_max = min(kRangeTok / 16, max_pages - (t0 >> 4));  // page ids past N_b are never used
   constexpr int kPgPerThr = kRangeTok / 16 / kScanNT;
@@ -813,7 +803,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 template <int G, class Sk, bool Pair, bool Two>
 __global__ void __launch_bounds__(Two ? 2 * kSelNT : kSelNT, Two ? 2 : 4) sbs_select_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
+    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     BudgetDev bud, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
     const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm, int ldw,
     float* __restrict__ scratch, int ld, int* __restrict__ counts_out, int force_fallback, int* __restrict__ err,
@@ -848,7 +838,7 @@ __global__ void __launch_bounds__(Two ? 2 * kSelNT : kSelNT, Two ? 2 : 4) sbs_se
   const int row_base = blockIdx.x * HPC;  // first q-row of the CTA (pairs are consecutive heads)
   const int b = row_base / Hq, g = (row_base - b * Hq) / G, j0 = row_base - b * Hq - g * G;
   const int bg = b * Hkv + g;
-  const int N = __ldg(seq_lens + b);
+  const int N = seq_len_dev(seq_lens, b, max_len);  // -1 / 0: SD_DEVERR_SEQLEN below
   const int* pt = page_table + (size_t)b * max_pages;
   for (int i = tid; i < HPC * C; i += NT) {  // (the q channels are used by the slow path only)
     const int hh = i / C, c = i - hh * C;
@@ -1137,13 +1127,13 @@ __global__ void __launch_bounds__(Two ? 2 * kSelNT : kSelNT, Two ? 2 : 4) sbs_se
 // --------------------------------------------------------------------------- 4. per-head index lists
 // Optional (idx_out requested): fbm row -> ascending token list.
 constexpr int kIdxNT = 256;
-__global__ void __launch_bounds__(kIdxNT) sbs_idx_kernel(const int* __restrict__ seq_lens, int Hq,
+__global__ void __launch_bounds__(kIdxNT) sbs_idx_kernel(const int* __restrict__ seq_lens, int max_len, int Hq,
                                                          const uint32_t* __restrict__ fbm, int ldw,
                                                          int* __restrict__ idx_out, int k_max_out) {
   __shared__ uint32_t warp_tot[33];
   const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
   pdl_wait();
-  const int N = __ldg(seq_lens + b);
+  const int N = seq_len_dev(seq_lens, b, max_len);
   const int nw = (max(N, 0) + 31) >> 5;
   const uint32_t* fr = fbm + (size_t)row * ldw;
   int* dst = idx_out + (size_t)row * k_max_out;
@@ -1164,8 +1154,8 @@ __global__ void __launch_bounds__(kIdxNT) sbs_idx_kernel(const int* __restrict__
 }
 
 template <class Kern>
-void set_smem(Kern k, size_t bytes) {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+cudaError_t set_smem(Kern k, size_t bytes) {
+  return ensure_dyn_smem(reinterpret_cast<const void*>(k), bytes);
 }
 
 template <class Kern, class... Args>
@@ -1210,18 +1200,19 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   {
     const size_t smem = sizeof(uint32_t) * G * (kHistWords + 512) + sizeof(float) * G * C + (size_t)G * kD * 4 +
                         sizeof(int) * C + sizeof(uint32_t) * G * 32;
-    const int snt = sample_threads(BG, geo.max_seq_len);
+    const int snt = sample_threads(BG, geo.max_seq_len, geo.sms);
     // few (b, g) rows: two CTAs per (b, g), half the heads each (fills more SMs)
     constexpr int GH = G >= 2 ? G / 2 : 1;
-    const bool split = G >= 2 && snt == kSampleThreads && 2 * BG <= sm_count();
+    const bool split = G >= 2 && snt == kSampleThreads && 2 * BG <= geo.sms;
     auto kern = snt == 512 ? sbs_sample_kernel<G, Sk, 512, G>
                            : split ? sbs_sample_kernel<G, Sk, kSampleThreads, GH> : sbs_sample_kernel<G, Sk, kSampleThreads, G>;
     const size_t smem_used = split ? sizeof(uint32_t) * GH * (kHistWords + 512) + sizeof(float) * GH * C + (size_t)GH * kD * 4 +
                                          sizeof(int) * C + sizeof(uint32_t) * GH * 32
                                    : smem;
-    set_smem(kern, smem_used);
+    e = set_smem(kern, smem_used);
+    if (e != cudaSuccess) return e;
     e = launch_pdl(kern, dim3(split ? 2 * BG : BG), dim3(snt), smem_used, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
-                   kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
+                   kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[0], st);
   }
@@ -1233,16 +1224,17 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     dim3 grid(nch, BG);
     // the fp8 sketch is C = 8 only (host-checked): no generic-C fp8 variant
     auto kern = C == 8 ? sbs_scan_kernel<G, true, Sk> : sbs_scan_kernel<G, false, SkBf16>;
-    set_smem(kern, smem);
+    e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
-                   geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch,
+                   geo.max_seq_len, geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch,
                    bud.dev());
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
   {
-    const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len));
+    const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len, geo.sms));
     const bool pair = SkMma<G, Sk>::value && C == 8;
     const size_t smem1 = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
     // two heads per CTA when that still fits 2 CTAs per SM (B*Hq/2 pairs in one wave)
@@ -1250,9 +1242,11 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     const size_t smem = two ? 2 * smem1 : smem1;
     auto kern = two ? sbs_select_kernel<G, Sk, true, true>
                     : pair ? sbs_select_kernel<G, Sk, true, false> : sbs_select_kernel<G, Sk, false, false>;
-    set_smem(kern, smem);
+    e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
     e = launch_pdl(kern, dim3(geo.B * geo.Hq / (two ? 2 : 1)), dim3(two ? 2 * kSelNT : kSelNT), smem, st, true, q,
-                   geo.kv_dtype, sk, skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_pages, geo.Hkv, bud.dev(),
+                   geo.kv_dtype, sk, skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages, geo.Hkv,
+                   bud.dev(),
                    (const uint32_t*)w.thr, (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch,
                    w.fbm, w.ldw, w.scratch, w.ld, w.counts_out, w.force_fallback, w.err, sel_cap);
     if (e != cudaSuccess) return e;
@@ -1278,7 +1272,7 @@ cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sket
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess || !w.idx_out) return e;
-  return launch_pdl(sbs_idx_kernel, dim3(g.B * g.Hq), dim3(kIdxNT), 0, st, true, kv.seq_lens, g.Hq,
+  return launch_pdl(sbs_idx_kernel, dim3(g.B * g.Hq), dim3(kIdxNT), 0, st, true, kv.seq_lens, g.max_seq_len, g.Hq,
                     (const uint32_t*)w.fbm, w.ldw, w.idx_out, w.k_max_out);
 }
 

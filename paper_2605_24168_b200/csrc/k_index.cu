@@ -17,11 +17,11 @@ template <int G, class Sk>
 __global__ void __launch_bounds__(kScanThreads) sketch_score_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk,
     const int* __restrict__ channel_ids, int C, const int* __restrict__ page_table,
-    const int* __restrict__ seq_lens, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
+    const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
   extern __shared__ float qc[];  // [G][C]
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
-  const int N = __ldg(seq_lens + b);
+  const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // invalid rows: not written (topk reports)
   for (int i = threadIdx.x; i < G * C; i += blockDim.x) {
     const int j = i / C, c = i - j * C;
     const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
@@ -51,12 +51,12 @@ __global__ void __launch_bounds__(kScanThreads) sketch_score_kernel(
 __global__ void __launch_bounds__(kScanThreads) sketch_score_mma_kernel(
     const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk,
     const int* __restrict__ channel_ids, const int* __restrict__ page_table,
-    const int* __restrict__ seq_lens, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
+    const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
   constexpr int G = 4, C = 8;
   __shared__ float qc[G * C];
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
-  const int N = __ldg(seq_lens + b);
+  const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // invalid rows: not written (topk reports)
   if (threadIdx.x < G * C) {
     const int j = threadIdx.x / C, c = threadIdx.x - j * C;
     const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
@@ -94,10 +94,10 @@ __global__ void __launch_bounds__(kScanThreads) sketch_score_mma_kernel(
 template <class KV, int G>
 __global__ void __launch_bounds__(kScanThreads) exact_score_kernel(
     const void* __restrict__ q, const void* __restrict__ kp, const int* __restrict__ page_table,
-    const int* __restrict__ seq_lens, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
+    const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
   const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
-  const int N = __ldg(seq_lens + b);
+  const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // invalid rows: not written (topk reports)
   const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
   float qf[G][8];
 #pragma unroll
@@ -132,21 +132,21 @@ cudaError_t index_dispatch(const Geo& g, const sd_paged_kv& kv, const sd_sketch*
     const size_t smem = sizeof(float) * G * sk->channels;
     if (sk->dtype == SD_E4M3)
       sketch_score_kernel<G, SkE4m3><<<grid, kScanThreads, smem, st>>>(
-          q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_pages, g.Hkv,
+          q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hkv,
           scores, ld);
     else if (G == 4 && sk->channels == 8)
       sketch_score_mma_kernel<<<grid, kScanThreads, 0, st>>>(
           q, g.kv_dtype, reinterpret_cast<const uint16_t*>(sk->pages), sk->channel_ids, kv.page_table, kv.seq_lens,
-          g.max_pages, g.Hkv, scores, ld);
+          g.max_seq_len, g.max_pages, g.Hkv, scores, ld);
     else
       sketch_score_kernel<G, SkBf16><<<grid, kScanThreads, smem, st>>>(
-          q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_pages, g.Hkv,
+          q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hkv,
           scores, ld);
   } else if (g.kv_dtype == SD_BF16) {
-    exact_score_kernel<KvBF16, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens,
+    exact_score_kernel<KvBF16, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens, g.max_seq_len,
                                                                  g.max_pages, g.Hkv, scores, ld);
   } else {
-    exact_score_kernel<KvF32, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens,
+    exact_score_kernel<KvF32, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens, g.max_seq_len,
                                                                 g.max_pages, g.Hkv, scores, ld);
   }
   return cudaGetLastError();

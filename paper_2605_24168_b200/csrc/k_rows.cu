@@ -48,8 +48,9 @@ __device__ __forceinline__ void lds_row8(const unsigned char* p, float* f) {
 template <class KV, int G, bool kDense>
 __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
     const void* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
-    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int max_tok) {
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
+    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int max_tok,
+    int* __restrict__ err) {
   using Cfg = RowCfg<KV>;
   constexpr int RB = Cfg::kRowBytes;
   constexpr int NS = Cfg::kStages;
@@ -84,7 +85,9 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
       for (int e = 0; e < 8; ++e) qf[j][e] *= scale_log2;
     }
   }
-  const int N = __ldg(seq_lens + b);
+  const int Nr = seq_len_dev(seq_lens, b, max_len);  // out of range: an empty row
+  if (kDense && Nr < 1 && split == 0 && g == 0 && threadIdx.x == 0) set_error(err, SD_DEVERR_SEQLEN);
+  const int N = max(Nr, 0);
   int T0, T1;
   if (kDense) {
     int per = (N + splits - 1) / splits;
@@ -239,14 +242,15 @@ __global__ void __launch_bounds__(kRowThreads) attend_rows_kernel(
 
 template <class KV, int G, bool kDense>
 cudaError_t launch_rows_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                          float scale, float* part, int splits, cudaStream_t st) {
+                          float scale, float* part, int splits, int* err, cudaStream_t st) {
   using Cfg = RowCfg<KV>;
   const int max_tok = kDense ? (((g.max_seq_len + splits - 1) / splits + 15) & ~15) : kRangeTok;
   const size_t smem = Cfg::kRingBytes + 2 * Cfg::kStages * sizeof(uint64_t) + sizeof(int) * (max_tok / 16 + 1) +
                       (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kRangeTok / 32) + 1)) + 16;
   static_assert((size_t)Cfg::kRingBytes >= (size_t)G * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
   auto kern = attend_rows_kernel<KV, G, kDense>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(splits, g.B * g.Hkv);
   cfg.blockDim = dim3(kRowThreads);
@@ -258,34 +262,35 @@ cudaError_t launch_rows_t(const Geo& g, const sd_paged_kv& kv, const void* q, co
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, q, reinterpret_cast<const char*>(kv.k_pages),
-                            reinterpret_cast<const char*>(kv.v_pages), kv.page_table, kv.seq_lens, g.max_pages,
-                            g.Hkv, fbm, ldw, scale * kLog2e, part, splits, max_tok);
+                            reinterpret_cast<const char*>(kv.v_pages), kv.page_table, kv.seq_lens, g.max_seq_len,
+                            g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits, max_tok, err);
 }
 
 template <class KV, bool kDense>
 cudaError_t launch_rows_g(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                          float scale, float* part, int splits, cudaStream_t st) {
+                          float scale, float* part, int splits, int* err, cudaStream_t st) {
   switch (g.G) {
-    case 1: return launch_rows_t<KV, 1, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
-    case 2: return launch_rows_t<KV, 2, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
-    case 4: return launch_rows_t<KV, 4, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
-    case 8: return launch_rows_t<KV, 8, kDense>(g, kv, q, fbm, ldw, scale, part, splits, st);
+    case 1: return launch_rows_t<KV, 1, kDense>(g, kv, q, fbm, ldw, scale, part, splits, err, st);
+    case 2: return launch_rows_t<KV, 2, kDense>(g, kv, q, fbm, ldw, scale, part, splits, err, st);
+    case 4: return launch_rows_t<KV, 4, kDense>(g, kv, q, fbm, ldw, scale, part, splits, err, st);
+    case 8: return launch_rows_t<KV, 8, kDense>(g, kv, q, fbm, ldw, scale, part, splits, err, st);
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
+// fp32 KV only (the bf16 paths run on the tensor cores: k_attend_pk.cu, k_rows_mma.cu)
 cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
                                float scale, float* part, int splits, cudaStream_t st) {
-  if (g.kv_dtype == SD_BF16) return launch_rows_g<KvBF16, false>(g, kv, q, fbm, ldw, scale, part, splits, st);
-  return launch_rows_g<KvF32, false>(g, kv, q, fbm, ldw, scale, part, splits, st);
+  if (g.kv_dtype != SD_F32) return cudaErrorInvalidValue;
+  return launch_rows_g<KvF32, false>(g, kv, q, fbm, ldw, scale, part, splits, nullptr, st);
 }
 
 cudaError_t launch_dense_rows(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
-                              int splits, cudaStream_t st) {
-  if (g.kv_dtype == SD_BF16) return launch_rows_g<KvBF16, true>(g, kv, q, nullptr, 0, scale, part, splits, st);
-  return launch_rows_g<KvF32, true>(g, kv, q, nullptr, 0, scale, part, splits, st);
+                              int splits, int* err, cudaStream_t st) {
+  if (g.kv_dtype != SD_F32) return cudaErrorInvalidValue;
+  return launch_rows_g<KvF32, true>(g, kv, q, nullptr, 0, scale, part, splits, err, st);
 }
 
 }  // namespace sd

@@ -1,5 +1,5 @@
-// k_rows_mma.cu - bf16 row-list gather-attend on tensor cores (A4/A5 of the
-// fused path over GQA union rows, and A7 dense decode).
+// k_rows_mma.cu - A7 dense decode (the in-repo baseline) on
+// the bf16 tensor cores.
 //
 // The G q-heads of one KV head share every gathered K/V row, so a 16-row tile
 // is a real dense contraction (BASELINE north_star: "tensor cores ... where the
@@ -11,17 +11,16 @@
 // keeps ~fp32 accuracy.  Rows a head did not select are masked to -inf before
 // the softmax (per-head selection bitmap of the CTA's token range).
 //
-// Union mode: each CTA owns tokens [T0, T0 + 4096) of one (b, g) and rebuilds
-// their ascending union rows from the selection description (sd_sbs.cuh).
+// Each CTA owns one contiguous token range of one (b, g).
 // Memory path: the range's page ids are cached in shared memory; rows are
 // streamed into a 3-stage shared ring with 16-B cp.async (LDGSTS; rows past
 // the end are zero-filled), XOR-swizzled per 16-B chunk so ldmatrix is
 // bank-conflict-free.  Each of the 4 warps owns 16 rows of every 64-row stage
 // and keeps its own online-softmax state; the 4 states are merged at the end
-// into one unnormalised split-k partial per q-head (merge_parts_kernel).
+// into one unnormalised split-k partial per q-head, and the last CTA of each
+// (b, g) merges the splits.
 #include "sd_common.cuh"
 #include "sd_internal.h"
-#include "sd_sbs.cuh"
 
 namespace sd {
 namespace {
@@ -76,37 +75,18 @@ __device__ __forceinline__ float bf16_round(float x) {
 // swizzled byte offset of 16-B chunk c of row r inside a [rows][256 B] block
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * kRowB + ((c ^ (r & 7)) << 4)); }
 
+constexpr int kStagesM = 3;  // ring depth (2 stages in flight)
+
 template <int G>
-struct AttTok {
-  static constexpr int value = 8192;  // tokens per union-mode CTA
-};
-constexpr int kBatchRows = 2048;      // union rows resolved into shared memory at a time
-
-// ring depth: 3 stages (2 in flight) for dense; 2 stages for union mode so
-// that 3 CTAs fit per SM and their per-range prologues overlap
-template <bool kDense>
-struct RingStages {
-  static constexpr int value = kDense ? 3 : 2;
-};
-
-template <int G, bool kDense>
 __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
-    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_pages, int Hkv,
-    const uint32_t* __restrict__ fbm, int ldw, float scale_log2, float* __restrict__ part, int splits, int max_tok,
-    void* __restrict__ out, int out_dtype, float* __restrict__ lse_out, int* __restrict__ counters) {
-  constexpr int kAtt = AttTok<G>::value;  // union mode: tokens per CTA
-  constexpr int kW = kAtt / 32;
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
+    float scale_log2, float* __restrict__ part, int splits, int max_tok, void* __restrict__ out, int out_dtype,
+    float* __restrict__ lse_out, int* __restrict__ counters, int* __restrict__ err) {
   constexpr uint32_t kAll = (1u << G) - 1u;
-  constexpr int kStagesM = RingStages<kDense>::value;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;                                                     // [stages][K | V]
   int* s_pages = reinterpret_cast<int*>(ring + kStagesM * kStageBytesM);          // [max_tok / 16 + 1]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(s_pages + max_tok / 16 + 1);         // [G][kW] head words
-  int* upre = reinterpret_cast<int*>(bm + (kDense ? 0 : G * kW));                // [kW + 1]
-  uint16_t* s_tok = reinterpret_cast<uint16_t*>(upre + (kDense ? 0 : kW + 1));   // [kBatchRows] token - T0
-  uint8_t* s_msk = reinterpret_cast<uint8_t*>(s_tok + (kDense ? 0 : kBatchRows));  // [kBatchRows]
-  __shared__ int warp_tot[kMmaWarps];
 
   const int bg = blockIdx.y, split = blockIdx.x;
   const int b = bg / Hkv, g = bg - b * Hkv;
@@ -126,28 +106,16 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
       qa2[kk] = *reinterpret_cast<const uint32_t*>(qrow + 8);
     }
   }
-  const int N = __ldg(seq_lens + b);
-  int T0, T1;  // token range of this CTA
-  if (kDense) {
-    int per = (N + splits - 1) / splits;
-    per = (per + 15) & ~15;
-    T0 = min(N, split * per);
-    T1 = min(N, T0 + per);
-  } else {
-    T0 = min(N, split * kAtt);
-    T1 = min(N, T0 + kAtt);
-  }
+  const int Nr = seq_len_dev(seq_lens, b, max_len);
+  if (Nr < 1 && split == 0 && tid == 0 && g == 0) set_error(err, SD_DEVERR_SEQLEN);  // row reads as empty
+  const int N = max(Nr, 0);
+  int per = (N + splits - 1) / splits;
+  per = (per + 15) & ~15;
+  const int T0 = min(N, split * per), T1 = min(N, T0 + per);  // token range of this CTA
   const int* pt = page_table + (size_t)b * max_pages;
   for (int i = tid; i < ((T1 - T0 + 15) >> 4); i += kMmaThreads) s_pages[i] = __ldg(pt + (T0 >> 4) + i);
-  const int nw = (T1 - T0 + 31) >> 5;
-  int total;
-  if (kDense) {
-    total = T1 - T0;
-    __syncthreads();
-  } else {
-    pdl_wait();  // the selection bitmaps come from sbs_select_kernel
-    total = T1 > T0 ? union_prologue<G, kMmaThreads>(fbm, ldw, b * Hq + g * G, T0, T1, bm, upre, warp_tot) : 0;
-  }
+  const int total = T1 - T0;
+  __syncthreads();
 
   // coalesced cp.async issue: thread tid copies 16-B chunk tid % 16 of rows
   // tid / 16 + 8 i (i < 8) of the K and V blocks; the swizzled destination
@@ -163,34 +131,8 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m = -INFINITY, lsum = 0.f;
 
-  // union rows are processed in batches of kBatchRows (one batch unless the
-  // selection is dense); dense mode is a single batch of contiguous rows
-  for (int rb = 0; rb < total; rb += kDense ? total : kBatchRows) {
-    const int nrows = kDense ? total : min(kBatchRows, total - rb);
-    if (!kDense) {
-      // resolve rows [rb, rb + nrows): each thread expands its words
-      __syncthreads();
-      for (int w = tid; w < nw; w += kMmaThreads) {
-        int pos = upre[w];
-        if (pos >= rb + nrows || upre[w + 1] <= rb) continue;
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < G; ++j) word |= bm[j * nw + w];
-        while (word) {
-          const int bit = __ffs(word) - 1;
-          word &= word - 1;
-          if (pos >= rb && pos < rb + nrows) {
-            uint32_t mk = 0;
-#pragma unroll
-            for (int j = 0; j < G; ++j) mk |= ((bm[j * nw + w] >> bit) & 1u) << j;
-            s_tok[pos - rb] = (uint16_t)(w * 32 + bit);
-            s_msk[pos - rb] = (uint8_t)mk;
-          }
-          ++pos;
-        }
-      }
-      __syncthreads();
-    }
+  {
+    const int nrows = total;
     const int nst = (nrows + kStageRowsM - 1) / kStageRowsM;
     auto issue = [&](int s) {
       if (s < nst) {
@@ -201,8 +143,7 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
           const bool valid = r < nrows;
           size_t off = 0;
           if (valid) {
-            const int tl = kDense ? r : (int)s_tok[r];
-            const int t = T0 + tl;
+            const int t = T0 + r;
             const uint32_t ri = (uint32_t)(s_pages[(t >> 4) - p0] * kPS + (t & 15)) * (uint32_t)Hkv + g;
             off = (size_t)ri * kRowB;
           }
@@ -242,7 +183,7 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int rr = rbase + nt * 8 + qc2 + e;
-            const uint32_t mk = rr < nrows ? (kDense ? kAll : (uint32_t)s_msk[rr]) : 0u;
+            const uint32_t mk = rr < nrows ? kAll : 0u;
             const bool ok = qr < G && ((mk >> qr) & 1u);
             x[nt * 2 + e] = ok ? sc[nt][e] * scale_log2 : -INFINITY;
           }
@@ -359,60 +300,35 @@ __global__ void __launch_bounds__(kMmaThreads) attend_rows_mma_kernel(
     }
     if (tid == 0) counters[bg] = 0;
   }
-  if (!kDense) pdl_launch_dependents();
 }
 
-template <int G, bool kDense>
-cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                         float scale, float* part, int splits, void* out, float* lse, int* counters,
-                         cudaStream_t st) {
-  constexpr int kAtt = AttTok<G>::value;
-  if (!kDense) splits = (g.max_seq_len + kAtt - 1) / kAtt;
-  const int max_tok = kDense ? (((g.max_seq_len + splits - 1) / splits + 15) & ~15) : kAtt;
-  constexpr int kStagesM = RingStages<kDense>::value;
-  const size_t smem = (size_t)kStagesM * kStageBytesM + sizeof(int) * (max_tok / 16 + 1) +
-                      (kDense ? 0 : sizeof(uint32_t) * ((G + 1) * (kAtt / 32) + 1) + 3 * kBatchRows) + 16;
+template <int G>
+cudaError_t launch_mma_t(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part, int splits,
+                         void* out, float* lse, int* counters, int* err, cudaStream_t st) {
+  const int max_tok = ((g.max_seq_len + splits - 1) / splits + 15) & ~15;
+  const size_t smem = (size_t)kStagesM * kStageBytesM + sizeof(int) * (max_tok / 16 + 1) + 16;
   static_assert(2 * kStageBytesM >= kMmaWarps * 8 * (kD + 2) * 4, "combine scratch must fit the ring");
-  auto kern = attend_rows_mma_kernel<G, kDense>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(splits, g.B * g.Hkv);
-  cfg.blockDim = dim3(kMmaThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = kDense ? 0 : 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint16_t*>(q),
-                            reinterpret_cast<const char*>(kv.k_pages), reinterpret_cast<const char*>(kv.v_pages),
-                            kv.page_table, kv.seq_lens, g.max_pages, g.Hkv, fbm, ldw, scale * kLog2e, part, splits,
-                            max_tok, out, g.out_dtype, lse, counters);
-}
-
-template <bool kDense>
-cudaError_t launch_mma_g(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
-                         float scale, float* part, int splits, void* out, float* lse, int* ctr, cudaStream_t st) {
-  switch (g.G) {
-    case 1: return launch_mma_t<1, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
-    case 2: return launch_mma_t<2, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
-    case 4: return launch_mma_t<4, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
-    case 8: return launch_mma_t<8, kDense>(g, kv, q, fbm, ldw, scale, part, splits, out, lse, ctr, st);
-  }
-  return cudaErrorInvalidValue;
+  auto kern = attend_rows_mma_kernel<G>;
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(splits, g.B * g.Hkv), kMmaThreads, smem, st>>>(
+      reinterpret_cast<const uint16_t*>(q), reinterpret_cast<const char*>(kv.k_pages),
+      reinterpret_cast<const char*>(kv.v_pages), kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hkv,
+      scale * kLog2e, part, splits, max_tok, out, g.out_dtype, lse, counters, err);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
-                                  int splits, void* out, float* lse, int* counters, cudaStream_t st) {
-  return launch_mma_g<true>(g, kv, q, nullptr, 0, scale, part, splits, out, lse, counters, st);
-}
-
-int union_att_splits(int G, int max_seq_len) {
-  const int t = AttTok<4>::value;
-  return (max_seq_len + t - 1) / t;
+                                  int splits, void* out, float* lse, int* counters, int* err, cudaStream_t st) {
+  switch (g.G) {
+    case 1: return launch_mma_t<1>(g, kv, q, scale, part, splits, out, lse, counters, err, st);
+    case 2: return launch_mma_t<2>(g, kv, q, scale, part, splits, out, lse, counters, err, st);
+    case 4: return launch_mma_t<4>(g, kv, q, scale, part, splits, out, lse, counters, err, st);
+    case 8: return launch_mma_t<8>(g, kv, q, scale, part, splits, out, lse, counters, err, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace sd

@@ -23,12 +23,12 @@ namespace {
 constexpr int kStNT = 1024;
 
 __global__ void __launch_bounds__(kStNT) stochastic_select_kernel(
-    const float* __restrict__ scores, const float* __restrict__ u, int ld, const int* __restrict__ seq_lens, int Hq,
+    const float* __restrict__ scores, const float* __restrict__ u, int ld, const int* __restrict__ seq_lens, int max_len, int Hq,
     int k_det, int n_samples, uint32_t* __restrict__ mark, int ldw, int* __restrict__ idx,
     float* __restrict__ weights, int* __restrict__ counts, int k_max, int* __restrict__ err) {
   __shared__ SelectSmem<kStNT> sm;
   const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
-  const int N = __ldg(seq_lens + b);
+  const int N = seq_len_dev(seq_lens, b, max_len);
   if (N < 0) {
     if (tid == 0) {
       set_error(err, SD_DEVERR_SEQLEN);
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kStNT) stochastic_select_kernel(
 cudaError_t launch_stochastic_select(const Geo& g, const float* scores, const float* u, int ld, const int* seq_lens,
                                      int k_det, int n_samples, uint32_t* mark, int ldw, int* idx, float* weights,
                                      int* counts, int k_max, int* err, cudaStream_t st) {
-  stochastic_select_kernel<<<g.B * g.Hq, kStNT, 0, st>>>(scores, u, ld, seq_lens, g.Hq, k_det, n_samples, mark, ldw,
+  stochastic_select_kernel<<<g.B * g.Hq, kStNT, 0, st>>>(scores, u, ld, seq_lens, g.max_seq_len, g.Hq, k_det, n_samples, mark, ldw,
                                                          idx, weights, counts, k_max, err);
   return cudaGetLastError();
 }

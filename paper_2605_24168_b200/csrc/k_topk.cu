@@ -21,13 +21,13 @@ constexpr int kTkThreads = 1024;
 // out_scores (nullable): the selected scores, same order as idx; slots
 // [count, k_max) of idx/out_scores are padded with -1 / -inf when pad != 0.
 __global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
-    const float* __restrict__ scores, int ld, const int* __restrict__ seq_lens,
-    const int* __restrict__ k_from, int Hq, BudgetDev bud, int* __restrict__ idx,
+    const float* __restrict__ scores, int ld, const int* __restrict__ seq_lens, int max_len,
+    const int* __restrict__ k_from, int max_from, int Hq, BudgetDev bud, int* __restrict__ idx,
     int* __restrict__ counts, float* __restrict__ out_scores, int k_max, int pad,
     int* __restrict__ err) {
   __shared__ SelectSmem<kTkThreads> sm;
   const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
-  const int N = __ldg(seq_lens + b);
+  const int N = seq_len_dev(seq_lens, b, max_len);  // -1: out of range (SEQLEN below)
   const bool regions = !k_from && budget_regions(bud);
   int k, lo = 0, hi = N;
   if (regions) {  // NEXT-1: sinks [0, lo) and locals [hi, N) rank above every score
@@ -36,13 +36,13 @@ __global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
     lo = rb.lo;
     hi = rb.hi;
   } else {
-    const int NK = k_from ? __ldg(k_from + b) : N;
-    k = (NK >= 1 && bud.S >= 1.f) ? budget_k_dev(NK, bud.S, bud.k_fixed) : 0;
-    if (k_from) k = min(k, N);
+    const int NK = k_from ? seq_len_dev(k_from, b, max_from) : N;
+    k = (NK >= 1 && (bud.k_fixed > 0 || bud.S >= 1.0)) ? budget_k_dev(NK, bud.S, bud.k_fixed) : 0;
+    if (k_from) k = NK >= 1 ? min(k, max(N, 0)) : -1;
   }
   int* out = idx + (size_t)row * k_max;
   float* osc = out_scores ? out_scores + (size_t)row * k_max : nullptr;
-  if (N < 0 || k > k_max || k > N || (k < 1 && !k_from && !regions) || (!k_from && !regions && bud.k_fixed > N)) {
+  if (N < 0 || k < 0 || k > k_max || k > N || (k < 1 && !k_from && !regions) || (!k_from && !regions && bud.k_fixed > N)) {
     if (tid == 0) { set_error(err, SD_DEVERR_SEQLEN); counts[row] = 0; }
     return;
   }
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
 // number to surv_cnt (may be 0).
 __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
     const float* __restrict__ all_cand, const int* __restrict__ cand_idx, int parts, int rank,
-    int rows, int Hq, const int* __restrict__ global_seq_lens, float S, int k_fixed, int k_max,
+    int rows, int Hq, const int* __restrict__ global_seq_lens, double S, int k_fixed, int k_max,
     int* __restrict__ surv, int* __restrict__ surv_cnt, int* __restrict__ err) {
   __shared__ SelectSmem<kTkThreads> sm;
   __shared__ uint32_t s_eq_before;
@@ -116,15 +116,16 @@ __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
 
 cudaError_t launch_topk(const Geo& g, const float* scores, int ld, const int* seq_lens,
                         Budget bud, int* idx, int* counts, int k_max, int* err, cudaStream_t st) {
-  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, nullptr, g.Hq, bud.dev(),
+  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, g.max_seq_len, nullptr, 0, g.Hq, bud.dev(),
                                                        idx, counts, nullptr, k_max, 0, err);
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const int* seq_lens,
-                              const int* global_lens, Budget bud, int* idx, int* counts,
+                              const int* global_lens, int max_global, Budget bud, int* idx, int* counts,
                               float* cand_scores, int k_max, int* err, cudaStream_t st) {
-  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, global_lens, g.Hq, bud.dev(),
+  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, g.max_seq_len, global_lens, max_global,
+                                                       g.Hq, bud.dev(),
                                                        idx, counts, cand_scores, k_max, 1,
                                                        err);
   return cudaGetLastError();

@@ -7,10 +7,27 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "sd_internal.h"
 
 namespace sd {
+
+cudaError_t ensure_dyn_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;  // (device, kernel) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({dev, kern});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[{dev, kern}] = bytes;
+  return e;
+}
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -115,6 +132,10 @@ sd_status check_geom(const sd_geometry* g, int max_seq_len, Geo* out) {
   out->kv_dtype = g->kv_dtype;
   out->out_dtype = g->out_dtype;
   out->max_seq_len = max_seq_len;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) ==
+      cudaSuccess && sms > 0)
+    out->sms = sms;
   return SD_OK;
 }
 
@@ -313,7 +334,7 @@ namespace {
 sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch, const void* q,
                      const sd_budget* budget, float scale, void* out, float* lse, int32_t* idx_out,
                      int32_t* counts_out, int32_t k_max_out, void* ws, size_t ws_bytes, sd_stream stream,
-                     cudaEvent_t* ev) {
+                     cudaEvent_t* ev, uint32_t flags) {
   SD_TRY(check_kv(kv, true));
   Geo g;
   SD_TRY(check_geom(geom, kv->max_seq_len, &g));
@@ -355,8 +376,7 @@ sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sk
   w.counts_out = counts_out;
   w.idx_out = idx_out;
   w.k_max_out = idx_out ? k_max_out : 0;
-  const char* ff = getenv("SD_FORCE_FALLBACK");
-  w.force_fallback = (ff && ff[0] == '1') ? 1 : 0;
+  w.force_fallback = (flags & SD_FUSED_FORCE_SLOW_PATH) ? 1 : 0;
   w.err = err;
   w.ev = ev ? ev + 1 : nullptr;
   if (ev) cudaEventRecord(ev[0], st);
@@ -384,7 +404,16 @@ sd_status sd_sparse_decode_fused(const sd_geometry* geom, const sd_paged_kv* kv,
                                  int32_t* idx_out, int32_t* counts_out, int32_t k_max_out, void* ws,
                                  size_t ws_bytes, sd_stream stream) {
   return fused_impl(geom, kv, sketch, q, budget, scale, out, lse, idx_out, counts_out, k_max_out, ws, ws_bytes,
-                    stream, nullptr);
+                    stream, nullptr, 0u);
+}
+
+sd_status sd_sparse_decode_fused_ex(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
+                                    const void* q, const sd_budget* budget, float scale, void* out, float* lse,
+                                    int32_t* idx_out, int32_t* counts_out, int32_t k_max_out, void* ws,
+                                    size_t ws_bytes, uint32_t flags, sd_stream stream) {
+  if (flags & ~(uint32_t)SD_FUSED_FORCE_SLOW_PATH) return SD_ERR_INVALID_ARG;
+  return fused_impl(geom, kv, sketch, q, budget, scale, out, lse, idx_out, counts_out, k_max_out, ws, ws_bytes,
+                    stream, nullptr, flags);
 }
 
 sd_status sd_sparse_decode_fused_timed(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch,
@@ -396,7 +425,7 @@ sd_status sd_sparse_decode_fused_timed(const sd_geometry* geom, const sd_paged_k
   for (int i = 0; i < 6; ++i)
     if (cudaEventCreate(&ev[i]) != cudaSuccess) return SD_ERR_CUDA;
   sd_status s = fused_impl(geom, kv, sketch, q, budget, scale, out, lse, nullptr, nullptr, 0, ws, ws_bytes, stream,
-                           ev);
+                           ev, 0u);
   if (s == SD_OK && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) s = SD_ERR_CUDA;
   for (int i = 0; i < n_phases; ++i) {
     phase_ms[i] = -1.f;
@@ -421,9 +450,10 @@ sd_status sd_dense_decode(const sd_geometry* geom, const sd_paged_kv* kv, const 
   if (mma) {
     int* ctr = reinterpret_cast<int*>(wsp(ws, L.ctr));
     SD_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * g.B * g.Hkv, st));  // merge counters
-    return cuda_status(launch_dense_rows_mma(g, *kv, q, scale, part, splits, out, lse, ctr, st));
+    return cuda_status(launch_dense_rows_mma(g, *kv, q, scale, part, splits, out, lse, ctr,
+                                             reinterpret_cast<int*>(ws), st));
   }
-  SD_CUDA(launch_dense_rows(g, *kv, q, scale, part, splits, st));
+  SD_CUDA(launch_dense_rows(g, *kv, q, scale, part, splits, reinterpret_cast<int*>(ws), st));
   return cuda_status(launch_merge_parts(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st));
 }
 
@@ -457,7 +487,7 @@ sd_status sd_seqshard_local_topk(const sd_geometry* geom, const sd_paged_kv* kv,
   int* counts = reinterpret_cast<int*>(wsp(ws, L.counts));
   const Budget bud = to_budget(budget);
   SD_CUDA(launch_index_score(g, *kv, sketch, q, scores, L.ld, st));
-  return cuda_status(launch_topk_shard(g, scores, L.ld, kv->seq_lens, global_seq_lens, bud, cand_idx,
+  return cuda_status(launch_topk_shard(g, scores, L.ld, kv->seq_lens, global_seq_lens, max_global_seq_len, bud, cand_idx,
                                        counts, cand_scores, k_max, err, st));
 }
 
@@ -465,7 +495,8 @@ sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv,
                                  const sd_budget* budget, const int32_t* global_seq_lens,
                                  const float* all_cand, const int32_t* cand_idx, int32_t k_max,
                                  int32_t parts, int32_t rank, float scale, float* part_o, float* part_lse,
-                                 void* ws, size_t ws_bytes, sd_stream stream) {
+                                 int32_t* surv_idx, int32_t* surv_counts, void* ws, size_t ws_bytes,
+                                 sd_stream stream) {
   SD_TRY(check_kv(kv, true));
   Geo g;
   SD_TRY(check_geom(geom, kv->max_seq_len, &g));
@@ -479,8 +510,8 @@ sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv,
   SD_TRY(check_ws(ws, ws_bytes, L.total));
   cudaStream_t st = (cudaStream_t)stream;
   int* err = reinterpret_cast<int*>(ws);
-  int* surv = reinterpret_cast<int*>(wsp(ws, L.idx));
-  int* surv_cnt = reinterpret_cast<int*>(wsp(ws, L.counts));
+  int* surv = surv_idx ? surv_idx : reinterpret_cast<int*>(wsp(ws, L.idx));
+  int* surv_cnt = surv_counts ? surv_counts : reinterpret_cast<int*>(wsp(ws, L.counts));
   const Budget bud = to_budget(budget);
   SD_CUDA(launch_seqshard_cut(g, all_cand, cand_idx, parts, rank, global_seq_lens, bud, k_max, surv,
                               surv_cnt, err, st));

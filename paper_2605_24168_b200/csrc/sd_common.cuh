@@ -23,11 +23,23 @@ __device__ __forceinline__ void set_error(int* err, int code) {
   if (err) atomicCAS(err, 0, code);
 }
 
+// ---------------------------------------------------------------- intake (A1)
+// N_b read against the HOST bound max_seq_len that sized the grids and the
+// workspace (sdattn.h: 1 <= N_b <= max_seq_len).  A length outside [0, max_len]
+// reads as -1: every kernel treats the row as empty (nothing is read or written
+// past the workspace rows) and the kernels that own the row's result report
+// SD_DEVERR_SEQLEN.  0 is returned as 0 (an empty local shard is legal for the
+// sequence-shard entries; the other entries reject it as SEQLEN).
+__device__ __forceinline__ int seq_len_dev(const int* __restrict__ seq_lens, int b, int max_len) {
+  const int n = __ldg(seq_lens + b);
+  return (n >= 0 && n <= max_len) ? n : -1;
+}
+
 // ---------------------------------------------------------------- budget (A1)
 // k_b = max(1, ceil(N / S)) in double precision, or k_fixed.
-__device__ __forceinline__ int budget_k_dev(int N, float S, int k_fixed) {
+__device__ __forceinline__ int budget_k_dev(int N, double S, int k_fixed) {
   if (k_fixed > 0) return k_fixed;
-  double q = (double)N / (double)S;
+  double q = (double)N / S;
   double c = ceil(q);
   int k = c < 1.0 ? 1 : (c > (double)N ? N : (int)c);
   return k;
@@ -41,15 +53,15 @@ __device__ __forceinline__ int budget_k_dev(int N, float S, int k_fixed) {
 // Implemented everywhere as "sink / local tokens score +inf" and a total
 // k = lo + (N - hi) + kh, so the selection stays a plain top-k.
 struct BudgetDev {
-  float S;
+  double S;
   int k_fixed, n_sink, n_local;
-  float heavy_fraction;
+  double heavy_fraction;
 };
 struct RowBudget {
   int lo, hi, k;  // middle region [lo, hi), total selected k (0 allowed in NEXT-1 mode)
 };
 __device__ __forceinline__ bool budget_regions(const BudgetDev& b) {
-  return b.n_sink != 0 || b.n_local != 0 || b.heavy_fraction != 0.f;
+  return b.n_sink != 0 || b.n_local != 0 || b.heavy_fraction != 0.0;
 }
 __device__ __forceinline__ RowBudget row_budget(int N, const BudgetDev& b) {
   RowBudget r;
@@ -64,7 +76,7 @@ __device__ __forceinline__ RowBudget row_budget(int N, const BudgetDev& b) {
   const int mid = r.hi - r.lo;
   int kh;
   if (b.k_fixed > 0) kh = min(b.k_fixed, mid);
-  else kh = min(mid, (int)floor((double)b.heavy_fraction * (double)mid + 0.5));
+  else kh = min(mid, (int)floor(b.heavy_fraction * (double)mid + 0.5));
   r.k = r.lo + (N - r.hi) + kh;
   return r;
 }
@@ -145,11 +157,6 @@ __device__ __forceinline__ void load_q8(const void* q, size_t elem, float* f) {
 // Element offset of row (page, slot, kv head g) in a [P][16][Hkv][128] pool.
 __device__ __forceinline__ size_t kv_row_elem(int page, int slot, int g, int Hkv) {
   return ((size_t)(page * kPS + slot) * Hkv + g) * kD;
-}
-
-// Physical (page, slot) of logical token t of sequence b.
-__device__ __forceinline__ int token_page(const int* __restrict__ page_table, int max_pages, int b, int t) {
-  return __ldg(page_table + (size_t)b * max_pages + (t >> 4));
 }
 
 // ---------------------------------------------------------------- output store

@@ -22,15 +22,21 @@ constexpr int band_region_cap(int G) { return G >= 8 ? 1024 : 128 * G; }
 struct Geo {
   int B, Hq, Hkv, G, max_pages, kv_dtype, out_dtype;
   int max_seq_len;
+  int sms = 148;  // SM count of the current device (grid sizing)
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) at most once per (device,
+// kernel, size): the only state the library keeps between calls is this
+// per-process cache of an idempotent driver setting (thread-safe).
+cudaError_t ensure_dyn_smem(const void* kern, size_t bytes);
+
 struct Budget {
-  float S;
+  double S;
   int k_fixed;
   int n_sink = 0, n_local = 0;
-  float heavy_fraction = 0.f;
+  double heavy_fraction = 0.0;
   BudgetDev dev() const { return BudgetDev{S, k_fixed, n_sink, n_local, heavy_fraction}; }
-  bool regions() const { return n_sink != 0 || n_local != 0 || heavy_fraction != 0.f; }
+  bool regions() const { return n_sink != 0 || n_local != 0 || heavy_fraction != 0.0; }
 };
 
 // Workspace carve-up; every region is 256-byte aligned.  Computed identically
@@ -71,15 +77,12 @@ cudaError_t launch_attend_list(const Geo& g, const sd_paged_kv& kv, const void* 
                                int allow_empty, int* err, cudaStream_t st);
 
 cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const int* seq_lens,
-                              const int* global_lens, Budget bud, int* idx, int* counts,
+                              const int* global_lens, int max_global, Budget bud, int* idx, int* counts,
                               float* cand_scores, int k_max, int* err, cudaStream_t st);
 
 cudaError_t launch_seqshard_cut(const Geo& g, const float* all_cand, const int* cand_idx, int parts,
                                 int rank, const int* global_lens, Budget bud, int k_max, int* surv,
                                 int* surv_cnt, int* err, cudaStream_t st);
-
-cudaError_t launch_dense(const Geo& g, const sd_paged_kv& kv, const void* q, float scale,
-                         float* part, int splits, cudaStream_t st);
 
 // Combine `splits` unnormalised partials per row into out / lse.
 cudaError_t launch_merge_parts(const float* part, int rows, int splits, void* out,
@@ -122,21 +125,20 @@ struct SbsBuffers {
 cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
                               Budget bud, const SbsBuffers& w, cudaStream_t st);
 
-// ---- row-list gather-attend (k_rows.cu: CUDA cores, k_rows_mma.cu: bf16 tensor cores)
+// ---- row-list gather-attend (k_rows.cu: fp32 KV on the CUDA cores; k_rows_mma.cu: bf16 dense decode on the tensor cores)
 cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
                                float scale, float* part, int splits, cudaStream_t st);
 cudaError_t launch_dense_rows(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
-                              int splits, cudaStream_t st);
+                              int splits, int* err, cudaStream_t st);
 // the bf16 tensor-core dense kernel folds the split merge into their last CTA per (b, g)
 // (counters: int32 [B*Hkv], zero between calls)
 cudaError_t launch_dense_rows_mma(const Geo& g, const sd_paged_kv& kv, const void* q, float scale, float* part,
-                                  int splits, void* out, float* lse, int* counters, cudaStream_t st);
+                                  int splits, void* out, float* lse, int* counters, int* err, cudaStream_t st);
 // persistent variant (k_attend_pk.cu); the split partials are merged by a
 // following merge_parts_kernel (PDL)
 cudaError_t launch_attend_union_pk(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
                                    float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st,
                                    cudaEvent_t ev_attend = nullptr);
-int union_att_splits(int G, int max_seq_len);
 int choose_row_splits(int groups, int rows_per_group, int resident_per_sm = 3);
 
 }  // namespace sd

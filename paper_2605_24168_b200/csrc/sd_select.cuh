@@ -140,82 +140,4 @@ __device__ __forceinline__ uint32_t emit_block(KeyAt key_at, int n, uint32_t tau
   return run_sel;
 }
 
-// One histogram pass over keys matching (prefix, pmask); returns the digit
-// holding the kr-th largest and the residual rank inside it (block-uniform).
-template <int NT, class KeyAt>
-__device__ __forceinline__ void radix_pass_block(KeyAt key_at, int n, uint32_t prefix, uint32_t pmask, int shift,
-                                                 int nb, uint32_t kr, SelectSmem<NT>& sm, uint32_t* digit,
-                                                 uint32_t* kr_out, bool build = true) {
-  const int tid = threadIdx.x;
-  if (build) {
-    for (int i = tid; i < 2048; i += NT) sm.hist[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < n; i += NT) {
-      const uint32_t key = key_at(i);
-      if ((key & pmask) == prefix) atomicAdd(&sm.hist[(key >> shift) & (nb - 1)], 1u);
-    }
-    __syncthreads();
-  }
-  const int per = (nb + NT - 1) / NT;
-  uint32_t local = 0;
-  for (int j = 0; j < per; ++j) {
-    const int bin = nb - 1 - (tid * per + j);
-    if (bin >= 0) local += sm.hist[bin];
-  }
-  uint32_t tot;
-  uint32_t above = block_excl_scan<NT>(local, sm.warp_tot, &tot);
-  for (int j = 0; j < per; ++j) {
-    const int bin = nb - 1 - (tid * per + j);
-    if (bin < 0) break;
-    const uint32_t c = sm.hist[bin];
-    if (above < kr && above + c >= kr) { sm.digit = (uint32_t)bin; sm.kr = kr - above; }
-    above += c;
-  }
-  __syncthreads();
-  *digit = sm.digit;
-  *kr_out = sm.kr;
-  __syncthreads();
-}
-
-// k-th largest key for two ranks ka, kb (1 <= ka, kb <= n) sharing the first
-// histogram pass (the sample bracket of the fused path).
-template <int NT, class KeyAt>
-__device__ __forceinline__ void radix_select2_block(KeyAt key_at, int n, uint32_t ka, uint32_t kb,
-                                                    SelectSmem<NT>& sm, uint32_t* tau_a, uint32_t* tau_b) {
-  uint32_t da, ra, db, rb;
-  radix_pass_block<NT>(key_at, n, 0u, 0u, 21, 2048, ka, sm, &da, &ra, true);
-  radix_pass_block<NT>(key_at, n, 0u, 0u, 21, 2048, kb, sm, &db, &rb, false);
-  uint32_t r[2] = {ra, rb}, pre[2] = {da << 21, db << 21}, out[2];
-#pragma unroll 1
-  for (int w = 0; w < 2; ++w) {
-    uint32_t prefix = pre[w], pmask = 0x7FFu << 21, kr = r[w], d;
-    radix_pass_block<NT>(key_at, n, prefix, pmask, 10, 2048, kr, sm, &d, &kr, true);
-    prefix |= d << 10;
-    pmask |= 0x7FFu << 10;
-    radix_pass_block<NT>(key_at, n, prefix, pmask, 0, 1024, kr, sm, &d, &kr, true);
-    out[w] = prefix | d;
-  }
-  *tau_a = out[0];
-  *tau_b = out[1];
-}
-
-// In-place ascending bitonic sort of n <= cap uint32 values in shared memory
-// (cap a power of two; slots [n, cap) must hold 0xFFFFFFFF).
-template <int NT>
-__device__ __forceinline__ void bitonic_sort_smem(uint32_t* a, int cap) {
-  for (int size = 2; size <= cap; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < cap / 2; i += NT) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const uint32_t x = a[lo], y = a[hi];
-        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
-      }
-    }
-  }
-  __syncthreads();
-}
-
 }  // namespace sd

@@ -59,6 +59,29 @@ def test_budget_matches_oracle(lib, S, N):
     assert k.value == oracle.budget_k(S, N)
 
 
+@pytest.mark.parametrize("S,N,want", [(1.3, 13, 10), (3.3, 33, 10), (2.3, 23, 10), (4.1, 41, 10)])
+def test_budget_non_representable_sparsity(lib, S, N, want):
+    """S is a double across the ABI: ceil(13 / 1.3) = 10 as in the SPEC's double
+    arithmetic.  Through a float32 field, 1.3f < 1.3 and 13 / 1.3f
+    = 10.0000004 would round up to 11 (likewise 33 / 3.3f, 23 / 2.3f, 41 / 4.1f)."""
+    from paper_2605_24168_b200 import _capi as C
+    k = C.c_i32()
+    assert lib.sd_budget_k(ctypes.byref(C.Budget(S, 0, 0, 0, 0.0)), N, ctypes.byref(k)) == 0
+    assert k.value == oracle.budget_k(S, N) == want
+
+
+@pytest.mark.parametrize("N,n_sink,n_local,hf,kh", [(5 + 8, 4, 4, 0.7, 4), (10 + 8, 4, 4, 0.45, 5),
+                                                    (10 + 8, 4, 4, 0.65, 7)])
+def test_heavy_fraction_non_representable(lib, N, n_sink, n_local, hf, kh):
+    """heavy_fraction is a double: round-half-up(0.7 * 5) = 4; through a
+    float32 field 0.7f * 5 = 3.49999994 would round to 3 (0.45f * 10 -> 4, 0.65f * 10 -> 6)."""
+    from paper_2605_24168_b200 import _capi as C
+    k = C.c_i32()
+    assert lib.sd_budget_k(ctypes.byref(C.Budget(1.0, 0, n_sink, n_local, hf)), N, ctypes.byref(k)) == 0
+    assert oracle.heavy_budget(N, n_sink, n_local, hf) == kh
+    assert k.value == n_sink + n_local + kh
+
+
 def test_budget_rejections(lib):
     from paper_2605_24168_b200 import _capi as C
     k = C.c_i32()
@@ -130,6 +153,13 @@ def test_validation_before_any_launch(lib):
     assert fused(_geom(C), kvv=C.PagedKV(None, fake, fake, fake, 128, 100)) == C.SD_ERR_INVALID_ARG
     assert fused(_geom(C), wsb=100) == C.SD_ERR_WORKSPACE
     assert fused(_geom(C), wsp=ctypes.c_void_p(0x10010)) == C.SD_ERR_WORKSPACE     # misaligned
+    # the option-flag entry: unknown flag bits are rejected before any launch
+    assert lib.sd_sparse_decode_fused_ex(ctypes.byref(_geom(C)), ctypes.byref(kv), ctypes.byref(sk), fake,
+                                         ctypes.byref(bud), 0.1, fake, None, None, None, 0, ws, 1 << 40, 2,
+                                         None) == C.SD_ERR_INVALID_ARG
+    assert lib.sd_sparse_decode_fused_ex(ctypes.byref(_geom(C, num_q_heads=30)), ctypes.byref(kv), ctypes.byref(sk),
+                                         fake, ctypes.byref(bud), 0.1, fake, None, None, None, 0, ws, 1 << 40,
+                                         C.SD_FUSED_FORCE_SLOW_PATH, None) == C.SD_ERR_INVALID_ARG
     assert lib.sd_lse_merge(0, 4, 128, fake, fake, 0, fake, None, None) == C.SD_ERR_INVALID_ARG
     assert lib.sd_lse_merge(2, 4, 64, fake, fake, 0, fake, None, None) == C.SD_ERR_UNSUPPORTED
 

@@ -12,8 +12,8 @@ import torch
 
 import oracle
 import workloads
-from parity import (OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_region_selection, check_selection, host_subcase,
-                    rel_err)
+from parity import (OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_region_selection, check_rows_full_size,
+                    check_selection, host_subcase, rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -278,6 +278,96 @@ def test_fused_sketch_matches_oracle(cuda_lib, dist):
     _check_fused(cuda_lib, case, 50.0, "sketch")
 
 
+@pytest.mark.parametrize("mode", ["sketch", "exact"])
+def test_fused_all_equal_keys_take_lowest_indices(cuda_lib, mode):
+    """S:204 (all scores equal, k = 3 -> {0, 1, 2}) at decode sizes: with every
+    key of a (sequence, KV head) identical, every row's selection must be
+    exactly the k_b lowest token indices - the only correct answer."""
+    sd = cuda_lib
+    lens = [1, 3, 100, 4099, 20000, 131072]
+    case = _dev(workloads.make_case(len(lens), 32, 8, lens, seed=29, dist="equal", sketch=mode == "sketch"))
+    kv, sk = _kv(sd, case)
+    sd.clear_device_error()
+    _, _, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk if mode == "sketch" else None, S=50.0, scale=SCALE,
+                                            return_idx=True)
+    assert sd.read_device_error() == 0
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b, N in enumerate(lens):
+        k = oracle.budget_k(50.0, N)
+        for h in range(case.Hq):
+            assert cnt[b, h] == k
+            assert np.array_equal(idx[b, h, :k], np.arange(k)), (b, h, idx[b, h, :8])
+
+
+@pytest.mark.parametrize("Hq,Hkv", [(32, 8), (8, 8), (16, 8), (16, 2)])
+@pytest.mark.parametrize("dist", ["iid", "needle", "dup", "spec"])
+@pytest.mark.parametrize("sketch_dtype", [torch.bfloat16, torch.float8_e4m3fn])
+def test_fused_selection_is_exact_topk_of_gpu_scores(cuda_lib, Hq, Hkv, dist, sketch_dtype):
+    """Where only one answer is correct it must be the one given: the fused
+    selection equals, bit for bit, oracle.topk_select (ties to the lower index,
+    S:200) applied to the GPU's own fp32 indexer scores (sd_sparse_index_score,
+    the same fp32 arithmetic).  dup plants exact ties that straddle tau."""
+    sd = cuda_lib
+    lens = [1, 100, 4099, 20000, 70001]
+    case = _dev(workloads.make_case(len(lens), Hq, Hkv, lens, seed=37 + Hq + Hkv, dist=dist, n_needles=64,
+                                    sketch_dtype=sketch_dtype))
+    kv, sk = _kv(sd, case)
+    sd.clear_device_error()
+    _, _, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, return_idx=True)
+    assert sd.read_device_error() == 0
+    sc = sd.sparse_index_score(case.q, kv, sk).cpu().numpy()
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b, N in enumerate(lens):
+        k = oracle.budget_k(50.0, N)
+        for h in range(Hq):
+            ref = oracle.topk_select(sc[b, h, :N].astype(np.float64), k)
+            assert cnt[b, h] == k
+            assert np.array_equal(idx[b, h, :k], ref), (b, h)
+
+
+def test_seq_len_above_max_seq_len_is_reported(cuda_lib):
+    """sdattn.h: N_b > max_seq_len (or < 1) is a device error (SD_DEVERR_SEQLEN);
+    the row reads as empty (out = 0, lse = -inf) and nothing else is touched:
+    the valid rows keep their exact results, for every entry point."""
+    sd = cuda_lib
+    host = workloads.make_case(3, 8, 2, [5000, 3000, 4000], seed=91)
+    case = _dev(host)
+    inp = oracle.from_case(host)
+    bad = torch.tensor([5000, 5001, 0], dtype=torch.int32, device="cuda")  # table rows hold 5008 tokens
+    kvb = sd.KVCache(case.k_pages, case.v_pages, case.page_table, bad, 5000)
+    sk = sd.SketchCache.from_case(case)
+
+    def ok_row0(out, lse, sel=None):
+        for h in range(8):
+            if sel is None:  # dense: attention over every row of sequence 0
+                ro, rl = oracle.attend_given(inp, 0, h, np.arange(5000), SCALE)
+            else:
+                ro, rl = oracle.attend_given(inp, 0, h, sel[h], SCALE)
+            assert rel_err(out[0, h], ro) <= 1e-4
+            check_lse(lse[0, h], rl)
+        assert np.all(out[1:] == 0) and np.all(np.isneginf(lse[1:]))
+
+    for mode in ("sketch", "exact"):
+        sd.clear_device_error()
+        out, lse, idx, cnt = sd.sparse_decode_fused(case.q, kvb, sk if mode == "sketch" else None, S=50.0,
+                                                    scale=SCALE, out_dtype=torch.float32, return_idx=True)
+        assert sd.read_device_error() == 5, mode
+        idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+        assert np.all(cnt[1:] == 0)
+        sels = {h: check_selection(idx[0, h], cnt[0, h], oracle.index_scores(inp, 0, h, mode), 100)
+                for h in range(8)}
+        ok_row0(out.cpu().numpy(), lse.cpu().numpy(), sels)
+    sd.clear_device_error()
+    out, lse = sd.dense_decode(case.q, kvb, scale=SCALE, out_dtype=torch.float32)
+    assert sd.read_device_error() == 5
+    ok_row0(out.cpu().numpy(), lse.cpu().numpy())
+    sd.clear_device_error()
+    sc = sd.sparse_index_score(case.q, kvb, sk)
+    _, cnt = sd.topk_select(sc, bad, 5000, S=50.0, num_kv_heads=2)
+    assert sd.read_device_error() == 5
+    assert np.all(cnt.cpu().numpy()[1:] == 0) and np.all(cnt.cpu().numpy()[0] == 100)
+
+
 @pytest.mark.parametrize("G,Hkv", [(1, 4), (2, 3), (8, 2)])
 @pytest.mark.parametrize("S", [2.0, 10.0, 50.0])
 def test_fused_sketch_group_sizes_and_sparsity(cuda_lib, G, Hkv, S):
@@ -442,29 +532,49 @@ def test_fused_equals_unfused_chain(cuda_lib):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["cfg2_s10", "cfg2_s100", "cfg3", "cfg4_t33", "cfg4_t66"])
-def test_fused_baseline_sizes_sampled_rows(cuda_lib, name):
-    """BASELINE.json full sizes in the bench's launch configuration; the oracle
-    checks sampled (b, h) rows one by one."""
+@pytest.mark.parametrize("name,heads", [("cfg3", "all"), ("cfg2_s10", 6), ("cfg2_s50", "all"), ("cfg2_s100", 6),
+                                        ("cfg4_t0", "all"), ("cfg4_t33", 6), ("cfg4_t66", 6)])
+def test_fused_baseline_sizes(cuda_lib, name, heads):
+    """BASELINE.json full sizes in the bench's launch configuration: for 2
+    sequences, every q-head ("all") or 6 sampled heads: the selection is the
+    exact top-k of the GPU's own fp32 scores (bit for bit) and within the
+    tolerance rule of the fp64 oracle scores; the output matches
+    oracle.attend_given on the GPU's selection."""
     sd = cuda_lib
     cfg = workloads.CONFIGS[name]
     case = workloads.config_case(name, device="cuda")
     kv, sk = _kv(sd, case)
+    sd.clear_device_error()
     out, lse, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk, S=cfg["S"], scale=SCALE,
                                                 out_dtype=torch.float32, return_idx=True)
-    torch.cuda.synchronize()
+    assert sd.read_device_error() == 0
+    assert sd.read_stats()["fallback_rows"] == 0
+    sc = sd.sparse_index_score(case.q, kv, sk)
+    out, lse, idx, cnt = out.cpu().numpy(), lse.cpu().numpy(), idx.cpu().numpy(), cnt.cpu().numpy()
     rng = np.random.default_rng(0)
     for b in rng.choice(case.B, 2, replace=False):
-        sub = host_subcase(case, int(b))
-        inp = oracle.from_case(sub)
-        N = int(case.seq_lens[b])
-        k = oracle.budget_k(cfg["S"], N)
-        for h in rng.choice(case.Hq, 3, replace=False):
-            scores = oracle.index_scores(inp, 0, int(h), "sketch")
-            sel = check_selection(idx[b, h].cpu().numpy(), int(cnt[b, h]), scores, k)
-            ro, rl = oracle.attend_given(inp, 0, int(h), sel, SCALE)
-            assert rel_err(out[b, h].cpu().numpy(), ro) <= 1e-4
-            check_lse(float(lse[b, h]), rl)
+        hs = list(range(case.Hq)) if heads == "all" else sorted(rng.choice(case.Hq, heads, replace=False).tolist())
+        check_rows_full_size(case, int(b), hs, cfg["S"], idx, cnt, out, lse, gpu_scores=sc[int(b)].cpu().numpy(),
+                             scale=SCALE)
+
+
+@pytest.mark.slow
+def test_fused_cfg5_geometry_one_gpu(cuda_lib):
+    """BASELINE cfg5's geometry unsharded on one GPU: B=1, Hq=32, Hkv=8,
+    N=2^20, S=100 (k=10486): fast path for every row, heads of four groups
+    checked bit-exactly on the GPU's scores and against the oracle."""
+    sd = cuda_lib
+    case = workloads.config_case("cfg5", device="cuda")
+    kv, sk = _kv(sd, case)
+    sd.clear_device_error()
+    out, lse, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk, S=100.0, scale=SCALE, out_dtype=torch.float32,
+                                                return_idx=True)
+    assert sd.read_device_error() == 0
+    assert sd.read_stats()["fallback_rows"] == 0
+    assert int(cnt.min()) == int(cnt.max()) == 10486
+    sc = sd.sparse_index_score(case.q, kv, sk)
+    check_rows_full_size(case, 0, [0, 13, 22, 31], 100.0, idx.cpu().numpy(), cnt.cpu().numpy(), out.cpu().numpy(),
+                         lse.cpu().numpy(), gpu_scores=sc[0].cpu().numpy(), scale=SCALE)
 
 
 @pytest.mark.parametrize("N,expect_fast", [(1 << 20, True), ((1 << 21) - 8192, None), ((1 << 21) + 4096, False)])
@@ -507,49 +617,73 @@ def _shard_kv(sd, case, lo, hi):
 
 
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_seqshard_protocol_equals_fused(cuda_lib, P):
-    """Local top-k per shard -> all candidates -> global cut + local attend ->
-    LSE merge equals the unsharded fused result (indices bit-exact)."""
+@pytest.mark.parametrize("dist", ["dup", "needle"])
+def test_seqshard_protocol_matches_oracle(cuda_lib, P, dist):
+    """Sequence sharding on one GPU: local top-k_b per shard ->
+    all candidate scores -> global cut + local attend -> LSE merge.  The union
+    of the ranks' survivors is bit for bit the exact top-k_b of the GPU's own
+    fp32 scores (duplicated keys: exact ties across shards go to the lower
+    global index) and equals oracle.seqshard_decode's index set; the merged
+    output matches oracle.seqshard_decode and oracle.attend_given on the set."""
     sd = cuda_lib
     N = 8192
-    case = _dev(workloads.make_case(2, 16, 4, [N, N], seed=50 + P, dist="dup"))
+    host = workloads.make_case(2, 16, 4, [N, N - 77], seed=50 + P, dist=dist, n_needles=40)
+    case = _dev(host)
     kv, sk = _kv(sd, case)
     S = 20.0
-    out_f, lse_f, idx_f, cnt_f = sd.sparse_decode_fused(case.q, kv, sk, S=S, scale=SCALE, out_dtype=torch.float32,
-                                                        return_idx=True)
-    bounds = [((r * N) // P) // 16 * 16 for r in range(P)] + [N]
     glens = case.seq_lens
     k_max = sd.budget_k(S, N)
+    bounds = [((r * N) // P) // 16 * 16 for r in range(P)] + [N]
     cands, cidx, kvs = [], [], []
     for r in range(P):
         kvr, _ = _shard_kv(sd, case, bounds[r], bounds[r + 1])
-        cs, ci = sd.seqshard_local_topk(case.q, kvr, sk and sd.SketchCache(sk.pages, sk.channel_ids), glens, N, S,
-                                        k_max=k_max)
+        cs, ci = sd.seqshard_local_topk(case.q, kvr, sk, glens, N, S, k_max=k_max)
         cands.append(cs)
         cidx.append(ci)
         kvs.append(kvr)
     all_cand = torch.stack(cands).contiguous()
-    parts_o, parts_l, surv = [], [], []
+    parts_o, parts_l, survs = [], [], []
     for r in range(P):
-        po, pl = sd.seqshard_cut_attend(case.q, kvs[r], glens, all_cand, cidx[r], r, S, scale=SCALE)
+        po, pl, sv, sc_ = sd.seqshard_cut_attend(case.q, kvs[r], glens, all_cand, cidx[r], r, S, scale=SCALE,
+                                                 return_survivors=True)
         parts_o.append(po)
         parts_l.append(pl)
+        survs.append((sv.cpu().numpy(), sc_.cpu().numpy()))
     out, lse = sd.lse_merge(torch.stack(parts_o).contiguous(), torch.stack(parts_l).contiguous())
-    assert (out - out_f).abs().max().item() <= 2e-5 * out_f.abs().max().item()
-    assert (lse - lse_f).abs().max().item() <= 1e-4
+    assert sd.read_device_error() == 0
+    out, lse = out.cpu().numpy(), lse.cpu().numpy()
+    gpu_sc = sd.sparse_index_score(case.q, kv, sk).cpu().numpy()
+    inp = oracle.from_case(host)
+    ref_idx, ref_o, ref_lse = oracle.seqshard_decode(inp, S, SCALE, P)
+    for b in range(case.B):
+        Nb = int(host.seq_lens[b])
+        k = oracle.budget_k(S, Nb)
+        for h in range(case.Hq):
+            got = np.sort(np.concatenate([sv[b, h, :c[b, h]] + bounds[r] for r, (sv, c) in enumerate(survs)]))
+            assert got.size == k
+            assert np.array_equal(got, oracle.topk_select(gpu_sc[b, h, :Nb].astype(np.float64), k)), (b, h)
+            check_selection(got, k, oracle.index_scores(inp, b, h, "sketch"), k)
+            assert np.array_equal(got, ref_idx[b][h]), (b, h)
+            assert rel_err(out[b, h], ref_o[b, h]) <= 1e-4, (b, h)
+            check_lse(lse[b, h], ref_lse[b, h])
+            ro, rl = oracle.attend_given(inp, b, h, got, SCALE)
+            assert rel_err(out[b, h], ro) <= 1e-4
+            check_lse(lse[b, h], rl)
 
 
 @pytest.mark.parametrize("dist", ["iid", "needle", "dup"])
-def test_fused_forced_fallback_identical(cuda_lib, dist, monkeypatch):
-    """The exact per-(b, g) fallback of the fused select gives the same index
-    sets and the same outputs as the sample-bracket fast path."""
+def test_fused_forced_fallback_identical(cuda_lib, dist):
+    """The exact per-(b, g) fallback of the fused select (sd_sparse_decode_fused_ex
+    with SD_FUSED_FORCE_SLOW_PATH) gives the same index sets and the same
+    outputs as the sample-bracket fast path."""
     sd = cuda_lib
     case = _dev(workloads.make_case(2, 32, 8, [20000, 3000], seed=61, dist=dist, n_needles=100))
     kv, sk = _kv(sd, case)
     a = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, out_dtype=torch.float32, return_idx=True)
-    monkeypatch.setenv("SD_FORCE_FALLBACK", "1")
-    b = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, out_dtype=torch.float32, return_idx=True)
-    monkeypatch.delenv("SD_FORCE_FALLBACK")
+    sd.clear_device_error()
+    b = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, out_dtype=torch.float32, return_idx=True,
+                               force_slow_path=True)
+    assert sd.read_stats()["fallback_rows"] == case.B * case.Hq
     assert torch.equal(a[3], b[3])
     for bb in range(2):
         for h in range(32):
