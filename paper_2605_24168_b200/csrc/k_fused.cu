@@ -376,6 +376,382 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   pdl_launch_dependents();
 }
 
+// --------------------------------------------------------------------------- select core (kernel 3.)
+// Arguments of the select step (the kernel parameter of sbs_select_kernel).
+struct SelArgs {
+  const void* q;
+  int q_dtype;
+  const void* sk;
+  const int* channel_ids;
+  int C;
+  const int* page_table;
+  const int* seq_lens;
+  int max_len, max_pages, Hkv;
+  BudgetDev bud;
+  const uint32_t* thr;
+  const uint32_t* ent_tok;
+  const float* ent_sc;
+  const int* ent_cnt;
+  int nch;
+  uint32_t* fbm;
+  int ldw;
+  float* scratch;
+  int ld;
+  int* counts_out;
+  int force_fallback;
+  int* err;
+  int sel_cap;
+};
+
+// the slow path's radix state and the fast path's band histograms share storage
+template <int NT, int HPC>
+union SelShared {
+  SelectSmem<NT> sel;
+  uint32_t hist2[HPC][kHistWords];
+};
+
+// Dynamic shared memory of select_core: keys, tokens [HPC][sel_cap], ties
+// [HPC][kTieCap], q channels [HPC][C].
+__host__ __device__ constexpr size_t sel_core_smem(int hpc, int sel_cap, int C) {
+  return (((size_t)4 * hpc * (2 * sel_cap + kTieCap + C)) + 127) & ~(size_t)127;
+}
+
+// The select of HPC consecutive q-rows row_base .. (one 256-thread group per
+// row); all NT = HPC * 256 threads of the CTA call it.  `smem` = dynamic shared
+// memory of at least sel_core_smem(HPC, sel_cap, C) bytes.
+template <int G, class Sk, bool Pair, bool Two>
+__device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsigned char* smem,
+                                            SelShared<(Two ? 2 : 1) * kSelNT, Two ? 2 : 1>& ush) {
+  const void* __restrict__ q = a.q;
+  const int q_dtype = a.q_dtype;
+  const void* __restrict__ sk = a.sk;
+  const int* __restrict__ channel_ids = a.channel_ids;
+  const int C = a.C;
+  const int* __restrict__ page_table = a.page_table;
+  const int* __restrict__ seq_lens = a.seq_lens;
+  const int max_len = a.max_len, max_pages = a.max_pages, Hkv = a.Hkv;
+  const BudgetDev bud = a.bud;
+  const uint32_t* __restrict__ thr = a.thr;
+  const uint32_t* __restrict__ ent_tok = a.ent_tok;
+  const float* __restrict__ ent_sc = a.ent_sc;
+  const int* __restrict__ ent_cnt = a.ent_cnt;
+  const int nch = a.nch;
+  uint32_t* __restrict__ fbm = a.fbm;
+  const int ldw = a.ldw;
+  float* __restrict__ scratch = a.scratch;
+  const int ld = a.ld;
+  int* __restrict__ counts_out = a.counts_out;
+  const int force_fallback = a.force_fallback;
+  int* __restrict__ err = a.err;
+  const int sel_cap = a.sel_cap;
+  // Two (tensor-core scan's head-pair regions, band capacity small enough for
+  // 2 CTAs per SM): one CTA per head pair, one 256-thread half per head; the
+  // pair's band entries are gathered once for both heads.  Otherwise one CTA
+  // per q-head.
+  static_assert(!Two || Pair, "two heads per CTA need head-pair regions");
+  constexpr int HPC = Two ? 2 : 1;    // heads per CTA
+  constexpr int NT = HPC * kSelNT;    // threads per CTA
+  constexpr int NW = kScanWarps;
+  constexpr int CW = band_region_cap(G);
+  uint32_t* keys0 = reinterpret_cast<uint32_t*>(smem);     // [HPC][sel_cap]
+  uint32_t* toks0 = keys0 + HPC * sel_cap;                 // [HPC][sel_cap]
+  uint32_t* ties0 = toks0 + HPC * sel_cap;                 // [HPC][kTieCap]
+  float* qc0 = reinterpret_cast<float*>(ties0 + HPC * kTieCap);  // [HPC][C]
+  SelectSmem<NT>& sm = ush.sel;
+  __shared__ int s_fb[HPC], s_sure[HPC], s_ntie[HPC], s_n[HPC];
+  __shared__ uint32_t s_pre[HPC], s_need[HPC];
+  __shared__ int s_shift[HPC], s_prev[HPC], s_done[HPC];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = tid / kSelNT, ht = tid - h * kSelNT, hw = ht >> 5;  // this thread's head slot / index in it
+  const int Hq = Hkv * G;
+  const int b = row_base / Hq, g = (row_base - b * Hq) / G, j0 = row_base - b * Hq - g * G;
+  const int bg = b * Hkv + g;
+  const int N = seq_len_dev(seq_lens, b, max_len);  // -1 / 0: SD_DEVERR_SEQLEN below
+  const int* pt = page_table + (size_t)b * max_pages;
+  for (int i = tid; i < HPC * C; i += NT) {  // (the q channels are used by the slow path only)
+    const int hh = i / C, c = i - hh * C;
+    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
+    qc0[i] = load_q_elem(q, q_dtype, (size_t)(row_base + hh) * kD + ch);
+  }
+  if (tid < HPC) {
+    s_fb[tid] = force_fallback;
+    s_sure[tid] = 0;
+    s_n[tid] = 0;
+  }
+  pdl_wait();
+  const RowBudget rb = row_budget(max(N, 0), bud);
+  const int k = N >= 1 ? rb.k : 0;
+  if (N < 1 || k > N || (k < 1 && !budget_regions(bud))) {
+    if (tid < HPC) {
+      set_error(err, SD_DEVERR_SEQLEN);
+      if (counts_out) counts_out[row_base + tid] = 0;
+    }
+    return;
+  }
+  const int row = row_base + h;  // this half's row
+  uint32_t* fr = fbm + (size_t)row * ldw;
+  const uint32_t lo = thr[row * 4 + 0], hi = thr[row * 4 + 1];
+  const int nw = (N + 31) >> 5;
+  __syncthreads();
+  // ---- sure count: the scan's bits of the half's row
+  {
+    int sure = 0;
+    for (int w = ht; w < nw; w += kSelNT) sure += __popc(fr[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
+    if (lane == 0 && sure) atomicAdd(&s_sure[h], sure);
+  }
+  // ---- band entries: warp per region over the whole CTA
+  int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
+  if (nreg > kTieCap - 1) {  // beyond 2M tokens: exact slow path
+    nreg = 0;
+    if (tid < HPC) s_fb[tid] = 1;
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  // band regions: union format (one per scan warp, G scores per entry) or, on
+  // the tensor-core scan (Pair), one per (scan warp, head pair) with the
+  // pair's 2 scores per entry
+  constexpr int nsub = Pair ? 2 : 1, nh = Pair ? 2 : G;
+  const int sub = Pair ? (j0 >> 1) : 0, e0 = Pair ? (j0 & 1) : j0;  // score index of head slot 0 (Two: 0)
+  const size_t reg0 = (size_t)bg * nch * NW;
+  auto greg = [&](int r) { return (reg0 + r) * nsub + sub; };
+  // region counts -> shared memory in one coalesced pass (overflow: slow path)
+  int* s_cnt = reinterpret_cast<int*>(ties0);  // reuse: [nreg]
+  for (int r = tid; r < nreg; r += NT) {
+    int c = ent_cnt[greg(r)];
+    if (c > CW) {
+      for (int hh = 0; hh < HPC; ++hh) s_fb[hh] = 1;
+      c = 0;
+    }
+    s_cnt[r] = c;
+  }
+  __syncthreads();
+  // warp per region with RQ regions in flight: entries lane + 32 u (u < UQ) of
+  // each are loaded before any is used; longer regions finish in a tail loop.
+  // Each entry is kept for every head slot whose mask bit it carries.
+  constexpr int RQ = 4, UQ = 2;
+  auto keep_group = [&](const uint32_t (&tk)[RQ][UQ], const float (&sc)[RQ][UQ][HPC], int nq) {
+#pragma unroll
+    for (int hh = 0; hh < HPC; ++hh) {
+      const uint32_t jbit = 1u << (24 + e0 + hh);
+      uint32_t* keys = keys0 + hh * sel_cap;
+      uint32_t* toks = toks0 + hh * sel_cap;
+      uint32_t bal[RQ][UQ];
+      int tot = 0;
+#pragma unroll
+      for (int qq = 0; qq < RQ; ++qq)
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) {
+          bal[qq][u] = qq < nq ? __ballot_sync(0xffffffffu, (tk[qq][u] & jbit) != 0u) : 0u;
+          tot += __popc(bal[qq][u]);
+        }
+      if (tot) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_n[hh], tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+        for (int qq = 0; qq < RQ; ++qq)
+#pragma unroll
+          for (int u = 0; u < UQ; ++u) {
+            const int p = base + __popc(bal[qq][u] & lt);
+            if ((bal[qq][u] >> lane) & 1u && p < sel_cap) {
+              keys[p] = score_key(sc[qq][u][hh]);
+              toks[p] = tk[qq][u] & 0x00FFFFFFu;
+            }
+            base += __popc(bal[qq][u]);
+          }
+      }
+    }
+  };
+  for (int rb0 = warp; rb0 < nreg; rb0 += (NT / 32) * RQ) {
+    uint32_t tk[RQ][UQ];
+    float sc[RQ][UQ][HPC];
+    int cnt[RQ];
+#pragma unroll
+    for (int qq = 0; qq < RQ; ++qq) {
+      const int r = rb0 + (NT / 32) * qq;
+      cnt[qq] = r < nreg ? s_cnt[r] : 0;
+      const uint32_t* rtok = ent_tok + greg(r) * CW;
+      const float* rsc = ent_sc + greg(r) * CW * nh + e0;
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) {
+        const int i = lane + 32 * u;
+        tk[qq][u] = i < cnt[qq] ? rtok[i] : 0u;
+        if constexpr (HPC == 2) {
+          const float2 v = i < cnt[qq] ? *reinterpret_cast<const float2*>(rsc + (size_t)i * nh) : make_float2(0.f, 0.f);
+          sc[qq][u][0] = v.x;
+          sc[qq][u][HPC - 1] = v.y;
+        } else {
+          sc[qq][u][0] = i < cnt[qq] ? rsc[(size_t)i * nh] : 0.f;
+        }
+      }
+    }
+    keep_group(tk, sc, RQ);
+    // tail: regions longer than 32 UQ entries
+    for (int qq = 0; qq < RQ; ++qq) {
+      const int r = rb0 + (NT / 32) * qq;
+      for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
+        uint32_t tk1[RQ][UQ] = {};
+        float sc1[RQ][UQ][HPC] = {};
+        const int i = i0 + lane;
+        if (i < cnt[qq]) {
+          tk1[0][0] = ent_tok[greg(r) * CW + i];
+#pragma unroll
+          for (int hh = 0; hh < HPC; ++hh) sc1[0][0][hh] = ent_sc[(greg(r) * CW + i) * nh + e0 + hh];
+        }
+        keep_group(tk1, sc1, 1);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- per head slot (one 256-thread half each, named barrier 1 + h): the
+  // exact r-th largest band key, ties, winners
+  auto hsync = [&]() {
+    if constexpr (HPC == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(kSelNT) : "memory");
+  };
+  uint32_t* keys = keys0 + h * sel_cap;
+  uint32_t* toks = toks0 + h * sel_cap;
+  uint32_t* ties = ties0 + h * kTieCap;
+  uint32_t* hist2 = ush.hist2[h];
+  const int n = s_n[h];
+  const int r_need = k - s_sure[h];
+  if (ht == 0 && (n > sel_cap || r_need < 0 || r_need > n)) s_fb[h] = 1;
+  hsync();
+  if (!s_fb[h] && r_need > 0) {
+    uint32_t tau;
+    int cut = INT_MAX;
+    // ---- adaptive radix select of the r-th largest band key (lo <= key <= hi)
+    if (ht == 0) {
+      const uint32_t span = hi - lo;
+      const int bits = span ? 32 - __clz(span) : 1;
+      s_prev[h] = bits;
+      s_shift[h] = bits > 11 ? bits - 11 : 0;
+      s_pre[h] = 0;
+      s_need[h] = (uint32_t)r_need;
+      s_done[h] = 0;
+    }
+    hsync();
+#pragma unroll 1
+    for (int pass = 0; pass < 3 && !s_done[h]; ++pass) {
+      for (int i = ht; i < kHistWords; i += kSelNT) hist2[i] = 0;
+      hsync();
+      const int sh = s_shift[h], prev = s_prev[h];
+      const uint32_t pre = s_pre[h], dmask = (1u << (prev - sh)) - 1u;
+      for (int i = ht; i < n; i += kSelNT) {
+        const uint32_t o = keys[i] - lo;
+        if ((uint32_t)((uint64_t)o >> prev) != pre) continue;
+        atomicAdd(&hist2[hidx((o >> sh) & dmask)], 1u);
+      }
+      hsync();
+      if (hw == 0) {
+        int bin;
+        uint32_t res;
+        warp_find_bin(hist2, s_need[h], &bin, &res);
+        if (lane == 0) {
+          s_pre[h] = (uint32_t)(((uint64_t)pre << (prev - sh)) | (uint32_t)bin);
+          s_need[h] = res;
+          s_prev[h] = sh;
+          s_shift[h] = sh > 11 ? sh - 11 : 0;
+          s_done[h] = sh == 0;
+        }
+      }
+      hsync();
+    }
+    tau = lo + s_pre[h];
+    const uint32_t need = s_need[h];
+    // ---- exact ties at tau: keep the lowest tokens if not all are needed
+    if (ht == 0) s_ntie[h] = 0;
+    hsync();
+    for (int i = ht; i < n; i += kSelNT) {
+      if (keys[i] == tau) {
+        const int p = atomicAdd(&s_ntie[h], 1);
+        if (p < kTieCap) ties[p] = toks[i];
+      }
+    }
+    hsync();
+    const int ntie = s_ntie[h];
+    if ((uint32_t)ntie > need) {
+      if (ntie > kTieCap) {
+        if (ht == 0) s_fb[h] = 1;
+      } else {
+        int cap2 = 1;
+        while (cap2 < ntie) cap2 <<= 1;
+        for (int i = ntie + ht; i < cap2; i += kSelNT) ties[i] = 0xFFFFFFFFu;
+        // ascending bitonic sort of the tied token ids (this half)
+        for (int size = 2; size <= cap2; size <<= 1) {
+          for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            hsync();
+            for (int i = ht; i < cap2 / 2; i += kSelNT) {
+              const int a = 2 * i - (i & (stride - 1)), c = a + stride;
+              const bool up = (a & size) == 0;
+              const uint32_t x = ties[a], y = ties[c];
+              if ((x > y) == up) {
+                ties[a] = y;
+                ties[c] = x;
+              }
+            }
+          }
+        }
+        hsync();
+        cut = (int)ties[need - 1];
+      }
+    }
+    hsync();
+    if (!s_fb[h]) {
+      // ---- band winners into the bitmap
+      for (int i = ht; i < n; i += kSelNT) {
+        const uint32_t key = keys[i];
+        const int t = (int)toks[i];
+        if (key > tau || (key == tau && t <= cut)) atomicOr(&fr[t >> 5], 1u << (t & 31));
+      }
+    }
+  }
+  __syncthreads();  // the halves join: the slow path uses the whole CTA
+  for (int hh = 0; hh < HPC; ++hh) {
+    if (!s_fb[hh]) continue;
+    // ---- exact slow path for row hh: zero the row, scores -> scratch, radix select, bitmap
+    const int rowh = row_base + hh, jh = j0 + hh;
+    uint32_t* frh = fbm + (size_t)rowh * ldw;
+    const float* qc = qc0 + hh * C;
+    if (tid == 0 && err) atomicAdd(err + 1, 1);  // statistics word: fallback rows
+    for (int w = tid; w < nw; w += NT) frh[w] = 0u;
+    float* sr = scratch + (size_t)rowh * ld;
+    if (SkMma<G, Sk>::value && C == 8) {  // the scan's tensor-core scores, same MMA placement
+      const SkMmaQ qm = sk_mma_q([qc, jh](int jj, int c) { return jj == jh ? qc[c] : 0.f; }, q_dtype == SD_F32 ? 3 : 1);
+      const int u = lane & 3, tofs = (lane >> 2) + ((u >> 1) << 4);
+      const bool mine = (u & 1) == (jh >> 1);
+      for (int t0 = warp * 32; t0 < N; t0 += NT) {
+        uint32_t a[4];
+        sk_mma_a_global(a, reinterpret_cast<const uint16_t*>(sk), t0, N,
+                        [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, 8); });
+        float d[4];
+        sk_mma_score(a, qm, d);
+        const int tA = t0 + tofs, tB = tA + 8;
+        const float vA = (jh & 1) ? d[1] : d[0], vB = (jh & 1) ? d[3] : d[2];
+        if (mine && tA < N) sr[tA] = (tA < rb.lo || tA >= rb.hi) ? INFINITY : vA;
+        if (mine && tB < N) sr[tB] = (tB < rb.lo || tB >= rb.hi) ? INFINITY : vB;
+      }
+    } else {
+      for (int t = tid; t < N; t += NT) {
+        const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+        float acc = 0.f;
+        for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1, Sk>(Sk::load8(sk, re + c0), qc + c0, C, &acc);
+        sr[t] = (t < rb.lo || t >= rb.hi) ? INFINITY : acc;
+      }
+    }
+    __syncthreads();
+    auto key_at = [sr](int i) { return score_key(sr[i]); };
+    uint32_t ftau, fneed;
+    radix_select_block<NT>(key_at, N, (uint32_t)k, sm, &ftau, &fneed);
+    emit_block<NT, 4>(key_at, N, ftau, fneed, 0u, sm,
+                      [frh](uint32_t, int i, uint32_t) { atomicOr(&frh[i >> 5], 1u << (i & 31)); });
+    __syncthreads();
+  }
+  if (counts_out && tid < HPC) counts_out[row_base + tid] = k;
+}
+
 // --------------------------------------------------------------------------- 2. scan
 // Every token of (b, g) is classified for each of the G q-heads by the bracket:
 //   sure  (key > hi):        its bit is set in the head's selection bitmap fbm
@@ -801,326 +1177,11 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 // or r > band, too many ties) the row is recomputed exactly the slow way into
 // a zeroed fbm row.
 template <int G, class Sk, bool Pair, bool Two>
-__global__ void __launch_bounds__(Two ? 2 * kSelNT : kSelNT, Two ? 2 : 4) sbs_select_kernel(
-    const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
-    int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
-    BudgetDev bud, const uint32_t* __restrict__ thr, const uint32_t* __restrict__ ent_tok,
-    const float* __restrict__ ent_sc, const int* __restrict__ ent_cnt, int nch, uint32_t* __restrict__ fbm, int ldw,
-    float* __restrict__ scratch, int ld, int* __restrict__ counts_out, int force_fallback, int* __restrict__ err,
-    int sel_cap) {
-  // Two (tensor-core scan's head-pair regions, band capacity small enough for
-  // 2 CTAs per SM): one CTA per head pair, one 256-thread half per head; the
-  // pair's band entries are gathered once for both heads.  Otherwise one CTA
-  // per q-head.
-  static_assert(!Two || Pair, "two heads per CTA need head-pair regions");
-  constexpr int HPC = Two ? 2 : 1;    // heads per CTA
-  constexpr int NT = HPC * kSelNT;    // threads per CTA
-  constexpr int NW = kScanWarps;
-  constexpr int CW = band_region_cap(G);
+__global__ void __launch_bounds__(Two ? 2 * kSelNT : kSelNT, Two ? 2 : 4) sbs_select_kernel(const SelArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t* keys0 = reinterpret_cast<uint32_t*>(smem);     // [HPC][sel_cap]
-  uint32_t* toks0 = keys0 + HPC * sel_cap;                 // [HPC][sel_cap]
-  uint32_t* ties0 = toks0 + HPC * sel_cap;                 // [HPC][kTieCap]
-  float* qc0 = reinterpret_cast<float*>(ties0 + HPC * kTieCap);  // [HPC][C]
-  // the slow path's radix state and the fast path's band histograms share storage
-  __shared__ union SelShared {
-    SelectSmem<NT> sel;
-    uint32_t hist2[HPC][kHistWords];
-  } ush;
-  SelectSmem<NT>& sm = ush.sel;
-  __shared__ int s_fb[HPC], s_sure[HPC], s_ntie[HPC], s_n[HPC];
-  __shared__ uint32_t s_pre[HPC], s_need[HPC];
-  __shared__ int s_shift[HPC], s_prev[HPC], s_done[HPC];
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = tid / kSelNT, ht = tid - h * kSelNT, hw = ht >> 5;  // this thread's head slot / index in it
-  const int Hq = Hkv * G;
-  const int row_base = blockIdx.x * HPC;  // first q-row of the CTA (pairs are consecutive heads)
-  const int b = row_base / Hq, g = (row_base - b * Hq) / G, j0 = row_base - b * Hq - g * G;
-  const int bg = b * Hkv + g;
-  const int N = seq_len_dev(seq_lens, b, max_len);  // -1 / 0: SD_DEVERR_SEQLEN below
-  const int* pt = page_table + (size_t)b * max_pages;
-  for (int i = tid; i < HPC * C; i += NT) {  // (the q channels are used by the slow path only)
-    const int hh = i / C, c = i - hh * C;
-    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
-    qc0[i] = load_q_elem(q, q_dtype, (size_t)(row_base + hh) * kD + ch);
-  }
-  if (tid < HPC) {
-    s_fb[tid] = force_fallback;
-    s_sure[tid] = 0;
-    s_n[tid] = 0;
-  }
-  pdl_wait();
-  const RowBudget rb = row_budget(max(N, 0), bud);
-  const int k = N >= 1 ? rb.k : 0;
-  if (N < 1 || k > N || (k < 1 && !budget_regions(bud))) {
-    if (tid < HPC) {
-      set_error(err, SD_DEVERR_SEQLEN);
-      if (counts_out) counts_out[row_base + tid] = 0;
-    }
-    return;
-  }
-  const int row = row_base + h;  // this half's row
-  uint32_t* fr = fbm + (size_t)row * ldw;
-  const uint32_t lo = thr[row * 4 + 0], hi = thr[row * 4 + 1];
-  const int nw = (N + 31) >> 5;
-  __syncthreads();
-  // ---- sure count: the scan's bits of the half's row
-  {
-    int sure = 0;
-    for (int w = ht; w < nw; w += kSelNT) sure += __popc(fr[w]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
-    if (lane == 0 && sure) atomicAdd(&s_sure[h], sure);
-  }
-  // ---- band entries: warp per region over the whole CTA
-  int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
-  if (nreg > kTieCap - 1) {  // beyond 2M tokens: exact slow path
-    nreg = 0;
-    if (tid < HPC) s_fb[tid] = 1;
-  }
-  const uint32_t lt = (1u << lane) - 1u;
-  // band regions: union format (one per scan warp, G scores per entry) or, on
-  // the tensor-core scan (Pair), one per (scan warp, head pair) with the
-  // pair's 2 scores per entry
-  constexpr int nsub = Pair ? 2 : 1, nh = Pair ? 2 : G;
-  const int sub = Pair ? (j0 >> 1) : 0, e0 = Pair ? (j0 & 1) : j0;  // score index of head slot 0 (Two: 0)
-  const size_t reg0 = (size_t)bg * nch * NW;
-  auto greg = [&](int r) { return (reg0 + r) * nsub + sub; };
-  // region counts -> shared memory in one coalesced pass (overflow: slow path)
-  int* s_cnt = reinterpret_cast<int*>(ties0);  // reuse: [nreg]
-  for (int r = tid; r < nreg; r += NT) {
-    int c = ent_cnt[greg(r)];
-    if (c > CW) {
-      for (int hh = 0; hh < HPC; ++hh) s_fb[hh] = 1;
-      c = 0;
-    }
-    s_cnt[r] = c;
-  }
-  __syncthreads();
-  // warp per region with RQ regions in flight: entries lane + 32 u (u < UQ) of
-  // each are loaded before any is used; longer regions finish in a tail loop.
-  // Each entry is kept for every head slot whose mask bit it carries.
-  constexpr int RQ = 4, UQ = 2;
-  auto keep_group = [&](const uint32_t (&tk)[RQ][UQ], const float (&sc)[RQ][UQ][HPC], int nq) {
-#pragma unroll
-    for (int hh = 0; hh < HPC; ++hh) {
-      const uint32_t jbit = 1u << (24 + e0 + hh);
-      uint32_t* keys = keys0 + hh * sel_cap;
-      uint32_t* toks = toks0 + hh * sel_cap;
-      uint32_t bal[RQ][UQ];
-      int tot = 0;
-#pragma unroll
-      for (int qq = 0; qq < RQ; ++qq)
-#pragma unroll
-        for (int u = 0; u < UQ; ++u) {
-          bal[qq][u] = qq < nq ? __ballot_sync(0xffffffffu, (tk[qq][u] & jbit) != 0u) : 0u;
-          tot += __popc(bal[qq][u]);
-        }
-      if (tot) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&s_n[hh], tot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-#pragma unroll
-        for (int qq = 0; qq < RQ; ++qq)
-#pragma unroll
-          for (int u = 0; u < UQ; ++u) {
-            const int p = base + __popc(bal[qq][u] & lt);
-            if ((bal[qq][u] >> lane) & 1u && p < sel_cap) {
-              keys[p] = score_key(sc[qq][u][hh]);
-              toks[p] = tk[qq][u] & 0x00FFFFFFu;
-            }
-            base += __popc(bal[qq][u]);
-          }
-      }
-    }
-  };
-  for (int rb0 = warp; rb0 < nreg; rb0 += (NT / 32) * RQ) {
-    uint32_t tk[RQ][UQ];
-    float sc[RQ][UQ][HPC];
-    int cnt[RQ];
-#pragma unroll
-    for (int qq = 0; qq < RQ; ++qq) {
-      const int r = rb0 + (NT / 32) * qq;
-      cnt[qq] = r < nreg ? s_cnt[r] : 0;
-      const uint32_t* rtok = ent_tok + greg(r) * CW;
-      const float* rsc = ent_sc + greg(r) * CW * nh + e0;
-#pragma unroll
-      for (int u = 0; u < UQ; ++u) {
-        const int i = lane + 32 * u;
-        tk[qq][u] = i < cnt[qq] ? rtok[i] : 0u;
-        if constexpr (HPC == 2) {
-          const float2 v = i < cnt[qq] ? *reinterpret_cast<const float2*>(rsc + (size_t)i * nh) : make_float2(0.f, 0.f);
-          sc[qq][u][0] = v.x;
-          sc[qq][u][HPC - 1] = v.y;
-        } else {
-          sc[qq][u][0] = i < cnt[qq] ? rsc[(size_t)i * nh] : 0.f;
-        }
-      }
-    }
-    keep_group(tk, sc, RQ);
-    // tail: regions longer than 32 UQ entries
-    for (int qq = 0; qq < RQ; ++qq) {
-      const int r = rb0 + (NT / 32) * qq;
-      for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
-        uint32_t tk1[RQ][UQ] = {};
-        float sc1[RQ][UQ][HPC] = {};
-        const int i = i0 + lane;
-        if (i < cnt[qq]) {
-          tk1[0][0] = ent_tok[greg(r) * CW + i];
-#pragma unroll
-          for (int hh = 0; hh < HPC; ++hh) sc1[0][0][hh] = ent_sc[(greg(r) * CW + i) * nh + e0 + hh];
-        }
-        keep_group(tk1, sc1, 1);
-      }
-    }
-  }
-  __syncthreads();
-  // ---- per head slot (one 256-thread half each, named barrier 1 + h): the
-  // exact r-th largest band key, ties, winners
-  auto hsync = [&]() {
-    if constexpr (HPC == 1) __syncthreads();
-    else asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(kSelNT) : "memory");
-  };
-  uint32_t* keys = keys0 + h * sel_cap;
-  uint32_t* toks = toks0 + h * sel_cap;
-  uint32_t* ties = ties0 + h * kTieCap;
-  uint32_t* hist2 = ush.hist2[h];
-  const int n = s_n[h];
-  const int r_need = k - s_sure[h];
-  if (ht == 0 && (n > sel_cap || r_need < 0 || r_need > n)) s_fb[h] = 1;
-  hsync();
-  if (!s_fb[h] && r_need > 0) {
-    uint32_t tau;
-    int cut = INT_MAX;
-    // ---- adaptive radix select of the r-th largest band key (lo <= key <= hi)
-    if (ht == 0) {
-      const uint32_t span = hi - lo;
-      const int bits = span ? 32 - __clz(span) : 1;
-      s_prev[h] = bits;
-      s_shift[h] = bits > 11 ? bits - 11 : 0;
-      s_pre[h] = 0;
-      s_need[h] = (uint32_t)r_need;
-      s_done[h] = 0;
-    }
-    hsync();
-#pragma unroll 1
-    for (int pass = 0; pass < 3 && !s_done[h]; ++pass) {
-      for (int i = ht; i < kHistWords; i += kSelNT) hist2[i] = 0;
-      hsync();
-      const int sh = s_shift[h], prev = s_prev[h];
-      const uint32_t pre = s_pre[h], dmask = (1u << (prev - sh)) - 1u;
-      for (int i = ht; i < n; i += kSelNT) {
-        const uint32_t o = keys[i] - lo;
-        if ((uint32_t)((uint64_t)o >> prev) != pre) continue;
-        atomicAdd(&hist2[hidx((o >> sh) & dmask)], 1u);
-      }
-      hsync();
-      if (hw == 0) {
-        int bin;
-        uint32_t res;
-        warp_find_bin(hist2, s_need[h], &bin, &res);
-        if (lane == 0) {
-          s_pre[h] = (uint32_t)(((uint64_t)pre << (prev - sh)) | (uint32_t)bin);
-          s_need[h] = res;
-          s_prev[h] = sh;
-          s_shift[h] = sh > 11 ? sh - 11 : 0;
-          s_done[h] = sh == 0;
-        }
-      }
-      hsync();
-    }
-    tau = lo + s_pre[h];
-    const uint32_t need = s_need[h];
-    // ---- exact ties at tau: keep the lowest tokens if not all are needed
-    if (ht == 0) s_ntie[h] = 0;
-    hsync();
-    for (int i = ht; i < n; i += kSelNT) {
-      if (keys[i] == tau) {
-        const int p = atomicAdd(&s_ntie[h], 1);
-        if (p < kTieCap) ties[p] = toks[i];
-      }
-    }
-    hsync();
-    const int ntie = s_ntie[h];
-    if ((uint32_t)ntie > need) {
-      if (ntie > kTieCap) {
-        if (ht == 0) s_fb[h] = 1;
-      } else {
-        int cap2 = 1;
-        while (cap2 < ntie) cap2 <<= 1;
-        for (int i = ntie + ht; i < cap2; i += kSelNT) ties[i] = 0xFFFFFFFFu;
-        // ascending bitonic sort of the tied token ids (this half)
-        for (int size = 2; size <= cap2; size <<= 1) {
-          for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            hsync();
-            for (int i = ht; i < cap2 / 2; i += kSelNT) {
-              const int a = 2 * i - (i & (stride - 1)), c = a + stride;
-              const bool up = (a & size) == 0;
-              const uint32_t x = ties[a], y = ties[c];
-              if ((x > y) == up) {
-                ties[a] = y;
-                ties[c] = x;
-              }
-            }
-          }
-        }
-        hsync();
-        cut = (int)ties[need - 1];
-      }
-    }
-    hsync();
-    if (!s_fb[h]) {
-      // ---- band winners into the bitmap
-      for (int i = ht; i < n; i += kSelNT) {
-        const uint32_t key = keys[i];
-        const int t = (int)toks[i];
-        if (key > tau || (key == tau && t <= cut)) atomicOr(&fr[t >> 5], 1u << (t & 31));
-      }
-    }
-  }
-  __syncthreads();  // the halves join: the slow path uses the whole CTA
-  for (int hh = 0; hh < HPC; ++hh) {
-    if (!s_fb[hh]) continue;
-    // ---- exact slow path for row hh: zero the row, scores -> scratch, radix select, bitmap
-    const int rowh = row_base + hh, jh = j0 + hh;
-    uint32_t* frh = fbm + (size_t)rowh * ldw;
-    const float* qc = qc0 + hh * C;
-    if (tid == 0 && err) atomicAdd(err + 1, 1);  // statistics word: fallback rows
-    for (int w = tid; w < nw; w += NT) frh[w] = 0u;
-    float* sr = scratch + (size_t)rowh * ld;
-    if (SkMma<G, Sk>::value && C == 8) {  // the scan's tensor-core scores, same MMA placement
-      const SkMmaQ qm = sk_mma_q([qc, jh](int jj, int c) { return jj == jh ? qc[c] : 0.f; }, q_dtype == SD_F32 ? 3 : 1);
-      const int u = lane & 3, tofs = (lane >> 2) + ((u >> 1) << 4);
-      const bool mine = (u & 1) == (jh >> 1);
-      for (int t0 = warp * 32; t0 < N; t0 += NT) {
-        uint32_t a[4];
-        sk_mma_a_global(a, reinterpret_cast<const uint16_t*>(sk), t0, N,
-                        [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, 8); });
-        float d[4];
-        sk_mma_score(a, qm, d);
-        const int tA = t0 + tofs, tB = tA + 8;
-        const float vA = (jh & 1) ? d[1] : d[0], vB = (jh & 1) ? d[3] : d[2];
-        if (mine && tA < N) sr[tA] = (tA < rb.lo || tA >= rb.hi) ? INFINITY : vA;
-        if (mine && tB < N) sr[tB] = (tB < rb.lo || tB >= rb.hi) ? INFINITY : vB;
-      }
-    } else {
-      for (int t = tid; t < N; t += NT) {
-        const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-        float acc = 0.f;
-        for (int c0 = 0; c0 < C; c0 += 8) sketch_fma8<1, Sk>(Sk::load8(sk, re + c0), qc + c0, C, &acc);
-        sr[t] = (t < rb.lo || t >= rb.hi) ? INFINITY : acc;
-      }
-    }
-    __syncthreads();
-    auto key_at = [sr](int i) { return score_key(sr[i]); };
-    uint32_t ftau, fneed;
-    radix_select_block<NT>(key_at, N, (uint32_t)k, sm, &ftau, &fneed);
-    emit_block<NT, 4>(key_at, N, ftau, fneed, 0u, sm,
-                      [frh](uint32_t, int i, uint32_t) { atomicOr(&frh[i >> 5], 1u << (i & 31)); });
-    __syncthreads();
-  }
-  if (counts_out && tid < HPC) counts_out[row_base + tid] = k;
+  __shared__ SelShared<(Two ? 2 : 1) * kSelNT, Two ? 2 : 1> ush;
+  // one CTA per q-row, or per head pair (consecutive heads)
+  select_core<G, Sk, Pair, Two>(a, blockIdx.x * (Two ? 2 : 1), smem, ush);
   pdl_launch_dependents();
 }
 
@@ -1217,6 +1278,11 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     if (w.ev) cudaEventRecord(w.ev[0], st);
   }
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
+  const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len, geo.sms));
+  const bool pair = SkMma<G, Sk>::value && C == 8;
+  SelArgs sa{q, geo.kv_dtype, sk, skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages,
+             geo.Hkv, bud.dev(), w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld,
+             w.counts_out, w.force_fallback, w.err, sel_cap};
   {
     const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 +
                         sizeof(float) * G * C + sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * (kRangeTok / 32) +
@@ -1234,24 +1300,18 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
   {
-    const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len, geo.sms));
-    const bool pair = SkMma<G, Sk>::value && C == 8;
-    const size_t smem1 = sizeof(uint32_t) * (2 * sel_cap + kTieCap) + sizeof(float) * C;
+    const size_t smem1 = sel_core_smem(1, sel_cap, C);
     // two heads per CTA when that still fits 2 CTAs per SM (B*Hq/2 pairs in one wave)
     const bool two = pair && 2 * smem1 + sizeof(uint32_t) * 2 * kHistWords + 4096 <= 113 * 1024;
-    const size_t smem = two ? 2 * smem1 : smem1;
+    const size_t smem = sel_core_smem(two ? 2 : 1, sel_cap, C);
     auto kern = two ? sbs_select_kernel<G, Sk, true, true>
                     : pair ? sbs_select_kernel<G, Sk, true, false> : sbs_select_kernel<G, Sk, false, false>;
     e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(kern, dim3(geo.B * geo.Hq / (two ? 2 : 1)), dim3(two ? 2 * kSelNT : kSelNT), smem, st, true, q,
-                   geo.kv_dtype, sk, skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages, geo.Hkv,
-                   bud.dev(),
-                   (const uint32_t*)w.thr, (const uint32_t*)w.ent_tok, (const float*)w.ent_sc, (const int*)w.ent_cnt, nch,
-                   w.fbm, w.ldw, w.scratch, w.ld, w.counts_out, w.force_fallback, w.err, sel_cap);
+    e = launch_pdl(kern, dim3(geo.B * geo.Hq / (two ? 2 : 1)), dim3(two ? 2 * kSelNT : kSelNT), smem, st, true, sa);
     if (e != cudaSuccess) return e;
-    if (w.ev) cudaEventRecord(w.ev[2], st);
   }
+  if (w.ev) cudaEventRecord(w.ev[2], st);
   return cudaSuccess;
 }
 
