@@ -55,6 +55,18 @@ constexpr int kSampleSlots = 4;            // sample tokens per thread
 static int sample_threads(int rows_bg, int max_seq_len, int sms) {
   return rows_bg > sms && max_seq_len <= 81920 ? 512 : kSampleThreads;
 }
+// The sample grows with N beyond 2^20 tokens: the bracket's band holds about
+// 8 sqrt(k / f) = 8 N / sqrt(S n_s) tokens, so n_s ~ N^2 keeps it within the
+// select's shared-memory band capacity.  Rounds of NT * kSampleSlots tokens:
+// 1 up to 2^20, ceil((N / 2^20)^2) beyond, at most kSampleMaxRounds (the fast
+// path then holds to 2^22 tokens at S = 100; longer rows take the exact slow path).
+constexpr int kSampleMaxRounds = 16;
+__host__ __device__ __forceinline__ int sample_rounds(int N) {
+  if (N <= (1 << 20)) return 1;
+  const double x = (double)N / (double)(1 << 20);
+  const int r = (int)ceil(x * x);
+  return r < kSampleMaxRounds ? r : kSampleMaxRounds;
+}
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
 constexpr int kScanStages = 3;
@@ -220,8 +232,9 @@ __device__ __forceinline__ void warp_find_bin256(const uint32_t* h, uint32_t r, 
 
 // GG = the GQA group size, G = the heads one CTA handles (GG / G CTAs per (b, g)
 // share the group's sample rows when there are few (b, g) rows).
-template <int GG, class Sk, int NT, int G>
-__global__ void __launch_bounds__(NT) sbs_sample_kernel(
+// MULTI: rows longer than 2^20 tokens possible (sample_rounds > 1).
+template <int GG, class Sk, int NT, int G, bool MULTI>
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_kernel(
     const void* __restrict__ q, int q_dtype, const void* __restrict__ sk, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     BudgetDev bud, uint32_t* __restrict__ thr, int* __restrict__ counters) {
@@ -237,6 +250,9 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   __shared__ uint32_t s_res[G][2];
   __shared__ uint32_t s_lohi[G][2];
   constexpr int kParts = GG / G;
+  // the scan grid may launch now: its CTAs stage their page ids and first
+  // sketch stages, then wait (griddepcontrol.wait) for this grid to complete
+  pdl_launch_dependents();
   const int part = blockIdx.x % kParts, bg = blockIdx.x / kParts, b = bg / Hkv, g = bg - b * Hkv;
   const int j0 = part * G;  // this CTA's heads: j0 .. j0 + G - 1 of the group
   const int Hq = Hkv * GG;
@@ -252,19 +268,24 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   const int N = seq_len_dev(seq_lens, b, max_len);  // < 1: an empty row (the select reports it)
   const int* pt = page_table + (size_t)b * max_pages;
   const int npg = (max(N, 1) + 15) >> 4;
-  const int cap_pages = CAP >> 4;
+  const int rounds = MULTI ? sample_rounds(max(N, 1)) : 1;
+  const int cap_pages = (CAP >> 4) * rounds;
   const int spg = (npg + cap_pages - 1) / cap_pages;  // page stride
   const int ns_pages = (npg + spg - 1) / spg;
   const int n_slots = ns_pages * 16;
   typename Sk::Raw raw[kSampleSlots];
   int tt[kSampleSlots];
+  // sample slot i = tid + NT u + CAP r of round r: token (i / 16) spg 16 + i % 16
+  auto load_round = [&](int r) {
 #pragma unroll
-  for (int u = 0; u < kSampleSlots; ++u) {
-    const int i = tid + u * NT;
-    const int t = (i >> 4) * spg * 16 + (i & 15);
-    tt[u] = (i < n_slots && t < N) ? t : -1;
-    if (tt[u] >= 0) raw[u] = Sk::load8(sk, sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
-  }
+    for (int u = 0; u < kSampleSlots; ++u) {
+      const int i = tid + u * NT + r * CAP;
+      const int t = (i >> 4) * spg * 16 + (i & 15);
+      tt[u] = (i < n_slots && t < N) ? t : -1;
+      if (tt[u] >= 0) raw[u] = Sk::load8(sk, sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C));
+    }
+  };
+  load_round(0);
   for (int i = tid; i < G * kHistWords; i += NT) hist1[i] = 0;
   for (int i = tid; i < G * 512; i += NT) hist2[i] = 0;
   if (tid < C) s_ch[tid] = chv;
@@ -283,28 +304,36 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
   const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
   const int k = min(rbud.k, N);
   uint32_t key[kSampleSlots][G];
+  auto score_round = [&]() {
 #pragma unroll
-  for (int u = 0; u < kSampleSlots; ++u) {
-    float acc[G];
+    for (int u = 0; u < kSampleSlots; ++u) {
+      float acc[G];
 #pragma unroll
-    for (int j = 0; j < G; ++j) acc[j] = 0.f;
-    if (tt[u] >= 0) {
-      sketch_fma8<G, Sk>(raw[u], qc, C, acc);
-      if (C > 8) {
-        const int t = tt[u];
-        const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
-        for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G, Sk>(Sk::load8(sk, re + c0), qc + c0, C, acc);
+      for (int j = 0; j < G; ++j) acc[j] = 0.f;
+      if (tt[u] >= 0) {
+        sketch_fma8<G, Sk>(raw[u], qc, C, acc);
+        if (C > 8) {
+          const int t = tt[u];
+          const size_t re = sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C);
+          for (int c0 = 8; c0 < C; c0 += 8) sketch_fma8<G, Sk>(Sk::load8(sk, re + c0), qc + c0, C, acc);
+        }
+        if (tt[u] < rbud.lo || tt[u] >= rbud.hi) {
+#pragma unroll
+          for (int j = 0; j < G; ++j) acc[j] = INFINITY;
+        }
       }
-      if (tt[u] < rbud.lo || tt[u] >= rbud.hi) {
 #pragma unroll
-        for (int j = 0; j < G; ++j) acc[j] = INFINITY;
-      }
+      for (int j = 0; j < G; ++j) key[u][j] = score_key(acc[j]);
     }
+  };
+  for (int r = 0; r < (MULTI ? rounds : 1); ++r) {
+    if (r) load_round(r);
+    score_round();
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      key[u][j] = score_key(acc[j]);
-      if (tt[u] >= 0) atomicAdd(&hist1[j * kHistWords + hidx(key[u][j] >> kSampleSh1)], 1u);
-    }
+    for (int u = 0; u < kSampleSlots; ++u)
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (tt[u] >= 0) atomicAdd(&hist1[j * kHistWords + hidx(key[u][j] >> kSampleSh1)], 1u);
   }
   const int last_sampled = (ns_pages - 1) * spg;
   const int n_s = n_slots - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
@@ -340,15 +369,21 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
     bin_lo[j] = s_bin1[j][0];
     bin_hi[j] = s_bin1[j][1];
   }
+  for (int r = 0; r < (MULTI ? rounds : 1); ++r) {
+    if (MULTI && rounds > 1) {  // one round: the keys are still in registers
+      load_round(r);
+      score_round();
+    }
 #pragma unroll
-  for (int u = 0; u < kSampleSlots; ++u) {
-    if (tt[u] < 0) continue;
+    for (int u = 0; u < kSampleSlots; ++u) {
+      if (tt[u] < 0) continue;
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const int b1 = (int)(key[u][j] >> kSampleSh1);
-      const uint32_t b2 = (key[u][j] >> kSampleSh2) & 255u;
-      if (b1 == bin_lo[j]) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
-      if (b1 == bin_hi[j]) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+      for (int j = 0; j < G; ++j) {
+        const int b1 = (int)(key[u][j] >> kSampleSh1);
+        const uint32_t b2 = (key[u][j] >> kSampleSh2) & 255u;
+        if (b1 == bin_lo[j]) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
+        if (b1 == bin_hi[j]) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+      }
     }
   }
   __syncthreads();
@@ -373,7 +408,6 @@ __global__ void __launch_bounds__(NT) sbs_sample_kernel(
     const float flo = thresh_lo(lo), fsure = hi == 0xFFFFFFFFu ? INFINITY : thresh_lo(hi + 1u);
     reinterpret_cast<uint4*>(thr)[row] = make_uint4(lo, hi, __float_as_uint(flo), __float_as_uint(fsure));
   }
-  pdl_launch_dependents();
 }
 
 // --------------------------------------------------------------------------- select core (kernel 3.)
@@ -401,6 +435,7 @@ struct SelArgs {
   int force_fallback;
   int* err;
   int sel_cap;
+  int nreg_cap;  // band regions the shared-memory count table holds (more: exact slow path)
 };
 
 // the slow path's radix state and the fast path's band histograms share storage
@@ -411,14 +446,14 @@ union SelShared {
 };
 
 // Dynamic shared memory of select_core: keys, tokens [HPC][sel_cap], ties
-// [HPC][kTieCap], q channels [HPC][C].
-__host__ __device__ constexpr size_t sel_core_smem(int hpc, int sel_cap, int C) {
-  return (((size_t)4 * hpc * (2 * sel_cap + kTieCap + C)) + 127) & ~(size_t)127;
+// [HPC][kTieCap], q channels [HPC][C], region counts [nreg_cap].
+__host__ __device__ constexpr size_t sel_core_smem(int hpc, int sel_cap, int C, int nreg_cap) {
+  return (((size_t)4 * hpc * (2 * sel_cap + kTieCap + C) + (size_t)4 * nreg_cap) + 127) & ~(size_t)127;
 }
 
 // The select of HPC consecutive q-rows row_base .. (one 256-thread group per
 // row); all NT = HPC * 256 threads of the CTA call it.  `smem` = dynamic shared
-// memory of at least sel_core_smem(HPC, sel_cap, C) bytes.
+// memory of at least sel_core_smem(HPC, sel_cap, C, nreg_cap) bytes.
 template <int G, class Sk, bool Pair, bool Two>
 __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsigned char* smem,
                                             SelShared<(Two ? 2 : 1) * kSelNT, Two ? 2 : 1>& ush) {
@@ -504,7 +539,7 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
   }
   // ---- band entries: warp per region over the whole CTA
   int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
-  if (nreg > kTieCap - 1) {  // beyond 2M tokens: exact slow path
+  if (nreg > a.nreg_cap) {  // count table too small (beyond the shared memory): exact slow path
     nreg = 0;
     if (tid < HPC) s_fb[tid] = 1;
   }
@@ -517,7 +552,7 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
   const size_t reg0 = (size_t)bg * nch * NW;
   auto greg = [&](int r) { return (reg0 + r) * nsub + sub; };
   // region counts -> shared memory in one coalesced pass (overflow: slow path)
-  int* s_cnt = reinterpret_cast<int*>(ties0);  // reuse: [nreg]
+  int* s_cnt = reinterpret_cast<int*>(qc0 + HPC * C);  // [nreg]
   for (int r = tid; r < nreg; r += NT) {
     int c = ent_cnt[greg(r)];
     if (c > CW) {
@@ -851,20 +886,10 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   for (int u = 0; u < (int)(sizeof(qv) / sizeof(uint4)); ++u)
     if (tid + u * kScanNT < nq16) qv[u] = __ldg(qsrc + tid + u * kScanNT);
   for (int i = tid; i < G * kWords; i += kScanNT) s_words[i] = 0u;
-  pdl_wait();  // the bracket comes from the sample kernel
-  float2 thv[G];  // {flo, fsure} per head, converted by the sample kernel
-#pragma unroll
-  for (int j = 0; j < G; ++j) thv[j] = __ldg(reinterpret_cast<const float2*>(thr) + 2 * (row0 + j) + 1);
-  if (t0 >= N) {
-    if (kMma) {
-      if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
-    } else if (lane == 0) {
-      ent_cnt[reg] = 0;
-    }
-    pdl_launch_dependents();
-    return;
-  }
-  const int ntok = min(N - t0, kRangeTok);
+  // the chunk's first ring stages do not depend on the sample kernel: they are
+  // requested before the PDL wait (the sample kernel lets this grid launch at
+  // its start), so the scan's first copies overlap the sample
+  const int ntok = max(0, min(N - t0, kRangeTok));
   // the q rows and channel ids are staged in the candidate area (unused until phase 1)
   unsigned char* s_qrow = reinterpret_cast<unsigned char*>(c_sc_all);        // [G][kD] q dtype
   int* s_ch = reinterpret_cast<int*>(s_qrow + (size_t)G * kD * 4);            // [C]
@@ -925,6 +950,21 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   };
 #pragma unroll
   for (int s = 0; s < kScanStages - 1; ++s) issue(s);
+  pdl_wait();  // the bracket comes from the sample kernel
+  float2 thv[G];  // {flo, fsure} per head, converted by the sample kernel
+  // (written by the PDL primary while this grid may already run: coherent
+  // L2 loads, not the read-only path)
+#pragma unroll
+  for (int j = 0; j < G; ++j) thv[j] = __ldcg(reinterpret_cast<const float2*>(thr) + 2 * (row0 + j) + 1);
+  if (ntok == 0) {
+    if (kMma) {
+      if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
+    } else if (lane == 0) {
+      ent_cnt[reg] = 0;
+    }
+    pdl_launch_dependents();
+    return;
+  }
 
   float qr[G][8];
   SkMmaQ qm;
@@ -1244,10 +1284,14 @@ int band_capacity(int max_seq_len, Budget bud, int sample_nt) {
   const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N)
                    : bud.regions() ? std::max(1.0, bud.heavy_fraction * N + bud.n_sink + bud.n_local)
                                    : std::ceil(N / bud.S);
-  const double f = std::min(1.0, (double)(sample_nt * kSampleSlots) / N);
+  const double f = std::min(1.0, (double)sample_rounds(max_seq_len) * sample_nt * kSampleSlots / N);
   const double sig = std::sqrt(k * f * (1.0 - f));
-  const double band = (2.0 * kBracketZ * sig + 2.0) / f;
-  const int cap = (int)std::min<double>(kSelCap, std::max(4096.0, 1.25 * band + 1024.0));
+  // the band spans dr sample ranks; the tokens between two sample order
+  // statistics dr ranks apart number dr / f with a relative spread ~ 1 / sqrt(dr)
+  const double dr = 2.0 * kBracketZ * sig + 2.0;
+  const double band = dr / f;
+  const double margin = 1.0 + 4.5 / std::sqrt(std::max(dr, 1.0));
+  const int cap = (int)std::min<double>(kSelCap, std::max(4096.0, band * margin + 256.0));
   return (cap + 255) & ~255;
 }
 
@@ -1265,8 +1309,12 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     // few (b, g) rows: two CTAs per (b, g), half the heads each (fills more SMs)
     constexpr int GH = G >= 2 ? G / 2 : 1;
     const bool split = G >= 2 && snt == kSampleThreads && 2 * BG <= geo.sms;
-    auto kern = snt == 512 ? sbs_sample_kernel<G, Sk, 512, G>
-                           : split ? sbs_sample_kernel<G, Sk, kSampleThreads, GH> : sbs_sample_kernel<G, Sk, kSampleThreads, G>;
+    const bool multi = sample_rounds(geo.max_seq_len) > 1;
+    auto kern = snt == 512 ? sbs_sample_kernel<G, Sk, 512, G, false>
+                : split ? (multi ? sbs_sample_kernel<G, Sk, kSampleThreads, GH, true>
+                                 : sbs_sample_kernel<G, Sk, kSampleThreads, GH, false>)
+                        : (multi ? sbs_sample_kernel<G, Sk, kSampleThreads, G, true>
+                                 : sbs_sample_kernel<G, Sk, kSampleThreads, G, false>);
     const size_t smem_used = split ? sizeof(uint32_t) * GH * (kHistWords + 512) + sizeof(float) * GH * C + (size_t)GH * kD * 4 +
                                          sizeof(int) * C + sizeof(uint32_t) * GH * 32
                                    : smem;
@@ -1280,9 +1328,13 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
   const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len, geo.sms));
   const bool pair = SkMma<G, Sk>::value && C == 8;
+  // the region count table: every band region of the longest row, unless the
+  // select's shared memory cannot hold it (those rows take the exact slow path)
+  int nreg_cap = nch * kScanWarps;
+  if (sel_core_smem(1, sel_cap, C, nreg_cap) + sizeof(SelShared<kSelNT, 1>) + 1024 > 227 * 1024) nreg_cap = 0;
   SelArgs sa{q, geo.kv_dtype, sk, skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages,
              geo.Hkv, bud.dev(), w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld,
-             w.counts_out, w.force_fallback, w.err, sel_cap};
+             w.counts_out, w.force_fallback, w.err, sel_cap, nreg_cap};
   {
     const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 +
                         sizeof(float) * G * C + sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * (kRangeTok / 32) +
@@ -1300,10 +1352,9 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }
   {
-    const size_t smem1 = sel_core_smem(1, sel_cap, C);
     // two heads per CTA when that still fits 2 CTAs per SM (B*Hq/2 pairs in one wave)
-    const bool two = pair && 2 * smem1 + sizeof(uint32_t) * 2 * kHistWords + 4096 <= 113 * 1024;
-    const size_t smem = sel_core_smem(two ? 2 : 1, sel_cap, C);
+    const bool two = pair && sel_core_smem(2, sel_cap, C, nreg_cap) + sizeof(uint32_t) * 2 * kHistWords + 4096 <= 113 * 1024;
+    const size_t smem = sel_core_smem(two ? 2 : 1, sel_cap, C, nreg_cap);
     auto kern = two ? sbs_select_kernel<G, Sk, true, true>
                     : pair ? sbs_select_kernel<G, Sk, true, false> : sbs_select_kernel<G, Sk, false, false>;
     e = set_smem(kern, smem);

@@ -90,7 +90,12 @@ __global__ void __launch_bounds__(kScanThreads) sketch_score_mma_kernel(
   }
 }
 
-// Exact scores from the K pages: one half-warp per token row.
+// Exact scores from the K pages: one half-warp per token row, kExUnroll rows
+// per half-warp in flight (their page ids, then their K rows, are requested
+// before any is used), kExTok tokens per CTA so that short rows still spread
+// over many SMs (BASELINE cfg1: N = 4096 on 16 CTAs instead of 2).
+constexpr int kExUnroll = 4;
+constexpr int kExTok = 256;
 template <class KV, int G>
 __global__ void __launch_bounds__(kScanThreads) exact_score_kernel(
     const void* __restrict__ q, const void* __restrict__ kp, const int* __restrict__ page_table,
@@ -99,27 +104,38 @@ __global__ void __launch_bounds__(kScanThreads) exact_score_kernel(
   const int Hq = Hkv * G;
   const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // invalid rows: not written (topk reports)
   const int l16 = threadIdx.x & 15, hw = threadIdx.x >> 4;
+  constexpr int NHW = kScanThreads / 16;
   float qf[G][8];
 #pragma unroll
   for (int j = 0; j < G; ++j) load_q8<KV>(q, ((size_t)b * Hq + g * G + j) * kD + l16 * 8, qf[j]);
   const int* pt = page_table + (size_t)b * max_pages;
-  const int tbeg = blockIdx.x * kScanTok;
-  const int tend = min(N, tbeg + kScanTok);
+  const int tbeg = blockIdx.x * kExTok;
+  const int tend = min(N, tbeg + kExTok);
   float* srow = scores + ((size_t)b * Hq + g * G) * ld;
   // uniform trip count per warp: both half-warps iterate together
-  for (int t0 = tbeg; t0 < tend; t0 += kScanThreads / 16) {
-    int t = t0 + hw;
-    const bool ok = t < tend;
-    if (!ok) t = tbeg;
-    float kf[8];
-    KV::unpack(KV::load(kp, kv_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv) + l16 * 8), kf);
+  for (int t0 = tbeg; t0 < tend; t0 += NHW * kExUnroll) {
+    int t[kExUnroll], pg[kExUnroll];
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      float s = 0.f;
+    for (int u = 0; u < kExUnroll; ++u) {
+      t[u] = t0 + hw + NHW * u;
+      pg[u] = __ldg(pt + ((t[u] < tend ? t[u] : tbeg) >> 4));
+    }
+    typename KV::Raw raw[kExUnroll];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s = fmaf(qf[j][e], kf[e], s);
-      s = half_warp_sum(s);
-      if (ok && l16 == j) srow[(size_t)j * ld + t] = s;
+    for (int u = 0; u < kExUnroll; ++u)
+      raw[u] = KV::load(kp, kv_row_elem(pg[u], (t[u] < tend ? t[u] : tbeg) & 15, g, Hkv) + l16 * 8);
+#pragma unroll
+    for (int u = 0; u < kExUnroll; ++u) {
+      float kf[8];
+      KV::unpack(raw[u], kf);
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s = fmaf(qf[j][e], kf[e], s);
+        s = half_warp_sum(s);
+        if (t[u] < tend && l16 == j) srow[(size_t)j * ld + t[u]] = s;
+      }
     }
   }
 }
@@ -143,9 +159,11 @@ cudaError_t index_dispatch(const Geo& g, const sd_paged_kv& kv, const sd_sketch*
           q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hkv,
           scores, ld);
   } else if (g.kv_dtype == SD_BF16) {
+    grid.x = (g.max_seq_len + kExTok - 1) / kExTok;
     exact_score_kernel<KvBF16, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens, g.max_seq_len,
                                                                  g.max_pages, g.Hkv, scores, ld);
   } else {
+    grid.x = (g.max_seq_len + kExTok - 1) / kExTok;
     exact_score_kernel<KvF32, G><<<grid, kScanThreads, 0, st>>>(q, kv.k_pages, kv.page_table, kv.seq_lens, g.max_seq_len,
                                                                 g.max_pages, g.Hkv, scores, ld);
   }

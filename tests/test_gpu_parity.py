@@ -572,19 +572,25 @@ def test_fused_cfg5_geometry_one_gpu(cuda_lib):
     assert sd.read_device_error() == 0
     assert sd.read_stats()["fallback_rows"] == 0
     assert int(cnt.min()) == int(cnt.max()) == 10486
+    # the band capacity holds the band's spread (~1/sqrt(sample ranks)) over many queries
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    for _ in range(8):
+        qx = torch.randn(case.q.shape, generator=g, device="cuda").to(case.q.dtype)
+        sd.sparse_decode_fused(qx, kv, sk, S=100.0, scale=SCALE)
+    torch.cuda.synchronize()
+    assert sd.read_stats()["fallback_rows"] == 0
     sc = sd.sparse_index_score(case.q, kv, sk)
     check_rows_full_size(case, 0, [0, 13, 22, 31], 100.0, idx.cpu().numpy(), cnt.cpu().numpy(), out.cpu().numpy(),
                          lse.cpu().numpy(), gpu_scores=sc[0].cpu().numpy(), scale=SCALE)
 
 
-@pytest.mark.parametrize("N,expect_fast", [(1 << 20, True), ((1 << 21) - 8192, None), ((1 << 21) + 4096, False)])
-def test_fused_maximum_lengths(cuda_lib, N, expect_fast):
-    """The fused path at the longest sequences: 2^20 (BASELINE cfg5 on one GPU,
-    fast path), the last length whose band-region table fits the select's
-    shared memory (2^21 - 8192: the 4096-token sample's bracket is then wider
-    than the band capacity for most rows, which take the exact slow path), and
-    beyond it (every row on the slow path).  Same results either way; sampled
-    rows checked one by one against the oracle."""
+@pytest.mark.parametrize("N", [1 << 20, (1 << 21) - 8192, (1 << 21) + 4096])
+def test_fused_maximum_lengths(cuda_lib, N):
+    """The fused path at the longest sequences: 2^20 (BASELINE cfg5 on one GPU)
+    and around 2^21, where the sample grows with N (rounds of 4096 tokens,
+    ~N^2) so the bracket's band stays within the select's capacity: every row
+    on the fast path.  Sampled rows checked one by one against the oracle."""
     sd = cuda_lib
     case = workloads.make_case(1, 8, 2, [N], seed=81, dist="needle", n_needles=16, device="cuda")
     kv, sk = _kv(sd, case)
@@ -593,9 +599,7 @@ def test_fused_maximum_lengths(cuda_lib, N, expect_fast):
                                                 return_idx=True)
     torch.cuda.synchronize()
     assert sd.read_device_error() == 0
-    fb = sd.read_stats()["fallback_rows"]
-    if expect_fast is not None:
-        assert (fb == 0) if expect_fast else (fb == case.Hq), fb
+    assert sd.read_stats()["fallback_rows"] == 0
     sub = host_subcase(case, 0)
     inp = oracle.from_case(sub)
     k = oracle.budget_k(100.0, N)
@@ -605,6 +609,27 @@ def test_fused_maximum_lengths(cuda_lib, N, expect_fast):
         ro, rl = oracle.attend_given(inp, 0, h, sel, SCALE)
         assert rel_err(out[0, h].cpu().numpy(), ro) <= 1e-4
         check_lse(float(lse[0, h]), rl)
+
+
+@pytest.mark.slow
+def test_fused_4m_tokens_fast_equals_slow(cuda_lib):
+    """2^22 tokens (16 sample rounds, the longest fast-path row at S = 100):
+    no row on the slow path, and the selection and outputs equal the forced
+    exact slow path (full-row radix select over the same fp32 scores) bit for bit."""
+    sd = cuda_lib
+    N = 1 << 22
+    case = workloads.make_case(1, 8, 2, [N], seed=83, device="cuda")
+    kv, sk = _kv(sd, case)
+    sd.clear_device_error()
+    o1, l1, i1, c1 = sd.sparse_decode_fused(case.q, kv, sk, S=100.0, scale=SCALE, out_dtype=torch.float32,
+                                            return_idx=True)
+    torch.cuda.synchronize()
+    assert sd.read_device_error() == 0
+    assert sd.read_stats()["fallback_rows"] == 0
+    o2, l2, i2, c2 = sd.sparse_decode_fused(case.q, kv, sk, S=100.0, scale=SCALE, out_dtype=torch.float32,
+                                            return_idx=True, force_slow_path=True)
+    assert torch.equal(c1, c2) and torch.equal(i1, i2)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
 # --------------------------------------------------------------------------- sequence sharding (1 GPU)
