@@ -410,6 +410,205 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_kernel(
   }
 }
 
+// Tensor-core variant for G = 4 q-heads per KV head, C = 8, bf16 sketch (the
+// scan's scoring, sd_score.cuh): a warp scores 32 sample tokens (two sampled
+// pages) for all 4 heads with one mma.sync, so the sample's scores are the
+// scan's bits.  H = heads this CTA brackets (4, or 2 when two CTAs share a
+// (b, g)).  Only keys >= 0 (positive scores) enter the level-1 histogram when
+// the highest rank needed is within the top quarter of the sample (keys below
+// cannot hold it; otherwise every key counts).  Same bracket statistics as
+// sbs_sample_kernel.
+template <int NT, int H, bool MULTI>
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_mma_kernel(
+    const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
+    BudgetDev bud, uint32_t* __restrict__ thr, int* __restrict__ counters) {
+  constexpr int GG = 4, C = 8;
+  constexpr int NWp = NT / 32;
+  constexpr int BPR = NWp * kSampleSlots;  // 32-token blocks per round
+  constexpr int CAP = BPR * 32;            // sample tokens per round (= NT * kSampleSlots)
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* hist1 = reinterpret_cast<uint32_t*>(smem);  // [H][kHistWords] padded 2048-bin
+  uint32_t* hist2 = hist1 + H * kHistWords;              // [H][2][256]
+  unsigned char* s_qrow = reinterpret_cast<unsigned char*>(hist2 + H * 512);  // [4][kD] q dtype
+  int* s_ch = reinterpret_cast<int*>(s_qrow + (size_t)GG * kD * 4);          // [C]
+  uint32_t* s_grp = reinterpret_cast<uint32_t*>(s_ch + C);                   // [H][32] level-1 group sums
+  __shared__ int s_bin1[H][2];
+  __shared__ uint32_t s_res[H][2];
+  __shared__ uint32_t s_lohi[H][2];
+  constexpr int kParts = GG / H;
+  pdl_launch_dependents();  // the scan may launch now (it waits for this grid before reading the bracket)
+  const int part = blockIdx.x % kParts, bg = blockIdx.x / kParts, b = bg / Hkv, g = bg - b * Hkv;
+  const int j0 = part * H;
+  const int Hq = Hkv * GG;
+  const int row0 = b * Hq + g * GG;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qb = q_dtype == SD_F32 ? 4 : 2;
+  const int chv = tid < C ? __ldg(channel_ids + (size_t)bg * C + tid) : 0;
+  const int nq16 = GG * kD * qb / 16;
+  const uint4* qsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)row0 * kD * qb);
+  const uint4 qv = tid < nq16 ? __ldg(qsrc + tid) : make_uint4(0u, 0u, 0u, 0u);
+  const int N = seq_len_dev(seq_lens, b, max_len);  // < 1: an empty row (the select reports it)
+  const int* pt = page_table + (size_t)b * max_pages;
+  const int npg = (max(N, 1) + 15) >> 4;
+  const int rounds = MULTI ? sample_rounds(max(N, 1)) : 1;
+  const int cap_pages = (CAP >> 4) * rounds;
+  const int spg = (npg + cap_pages - 1) / cap_pages;  // page stride
+  const int ns_pages = (npg + spg - 1) / spg;
+  // lane (r, uu) of the MMA: A rows r, r + 8 (page 2 bi) and r, r + 8 (page 2 bi + 1), channels 2 uu, 2 uu + 1;
+  // D: tokens tA = r + 16 (uu >> 1), tA + 8 of the block, heads 2 (uu & 1), 2 (uu & 1) + 1
+  const int r = lane >> 2, uu = lane & 3;
+  uint32_t a[kSampleSlots][4];
+  int tA[kSampleSlots];  // absolute token of D rows r (+16) of block slot u; -1: block not sampled
+  auto load_round = [&](int rr) {
+    int pg[kSampleSlots][2];
+#pragma unroll
+    for (int u = 0; u < kSampleSlots; ++u) {
+      const int bi = warp + NWp * u + BPR * rr;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int sp = 2 * bi + e;
+        pg[u][e] = sp < ns_pages ? __ldg(pt + sp * spg) : -1;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSampleSlots; ++u) {
+      const int bi = warp + NWp * u + BPR * rr;
+      tA[u] = 2 * bi < ns_pages ? (2 * bi + (uu >> 1)) * spg * 16 + r : -1;
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm) {
+        const int e = mm >> 1, slot = 8 * (mm & 1) + r;
+        const int t = (2 * bi + e) * spg * 16 + slot;
+        a[u][mm] = (pg[u][e] >= 0 && t < N)
+                       ? __ldg(reinterpret_cast<const uint32_t*>(sk + sketch_row_elem(pg[u][e], slot, g, Hkv, C)) + uu)
+                       : 0u;
+      }
+    }
+  };
+  load_round(0);
+  for (int i = tid; i < H * kHistWords; i += NT) hist1[i] = 0;
+  for (int i = tid; i < H * 512; i += NT) hist2[i] = 0;
+  if (tid < C) s_ch[tid] = chv;
+  if (tid < nq16) reinterpret_cast<uint4*>(s_qrow)[tid] = qv;
+  if (tid == 0) {
+    if (part == 0) counters[bg] = 0;  // re-arm the gather-attend merge counter of (b, g)
+    if (blockIdx.x == 0) counters[gridDim.x / kParts] = 0;  // and the work counter
+  }
+  __syncthreads();
+  if (N < 1) return;
+  const SkMmaQ qm = sk_mma_q(
+      [&](int j, int c) {
+        const int e = j * kD + s_ch[c];
+        return qb == 4 ? reinterpret_cast<const float*>(s_qrow)[e] : bf_lo(reinterpret_cast<const uint16_t*>(s_qrow)[e]);
+      },
+      q_dtype == SD_F32 ? 3 : 1);
+  const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
+  const int k = min(rbud.k, N);
+  const int last_sampled = (ns_pages - 1) * spg;
+  const int n_s = ns_pages * 16 - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
+  int r_lo, r_hi;
+  if (n_s >= N) {
+    r_lo = r_hi = k;
+  } else {
+    const double f = (double)n_s / (double)N;
+    const double mu = (double)k * f, sd = sqrt((double)k * f * (1.0 - f));
+    r_lo = (int)ceil(mu + kBracketZ * sd + 1.0);
+    r_hi = (int)floor(mu - kBracketZ * sd);
+  }
+  const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
+  const uint32_t kmin = 4u * ra <= (uint32_t)n_s ? 0x80000000u : 0u;  // level-1 key floor
+  const int hsel = 2 * (uu & 1) - j0;  // this lane's first head, relative to the CTA's
+  const bool mine = hsel >= 0 && hsel < H;
+  uint32_t key[kSampleSlots][4];  // [u][(token tA | tA + 8) * 2 + head]
+  auto score_round = [&]() {
+#pragma unroll
+    for (int u = 0; u < kSampleSlots; ++u) {
+      float d[4];
+      sk_mma_score(a[u], qm, d);
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int t = tA[u] + 8 * (x >> 1);
+        if (t >= 0 && (t < rbud.lo || t >= rbud.hi)) d[x] = INFINITY;
+        key[u][x] = (tA[u] >= 0 && t < N) ? score_key(d[x]) : 0u;  // 0: not a sample token
+      }
+    }
+  };
+  for (int rr = 0; rr < (MULTI ? rounds : 1); ++rr) {
+    if (rr) load_round(rr);
+    score_round();
+    if (mine) {
+#pragma unroll
+      for (int u = 0; u < kSampleSlots; ++u)
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          if (key[u][x] >= kmin && key[u][x] != 0u)
+            atomicAdd(&hist1[(hsel + (x & 1)) * kHistWords + hidx(key[u][x] >> kSampleSh1)], 1u);
+    }
+  }
+  __syncthreads();
+  hist_group_sums<NT>(hist1, H, s_grp);
+  __syncthreads();
+  if (warp < 2 * H) {
+    const int j = warp >> 1, e = warp & 1;
+    int bin;
+    uint32_t res;
+    warp_find_bin(hist1 + j * kHistWords, e ? rb : ra, &bin, &res, s_grp + j * 32);
+    if (lane == 0) {
+      s_bin1[j][e] = bin;
+      s_res[j][e] = res;
+    }
+  }
+  __syncthreads();
+  // level 2: the next 8 key bits inside the two bins of each head
+  int bl0 = 0, bh0 = 0, bl1 = 0, bh1 = 0;
+  if (mine) {
+    bl0 = s_bin1[hsel][0];
+    bh0 = s_bin1[hsel][1];
+    bl1 = s_bin1[hsel + 1][0];
+    bh1 = s_bin1[hsel + 1][1];
+  }
+  for (int rr = 0; rr < (MULTI ? rounds : 1); ++rr) {
+    if (MULTI && rounds > 1) {  // one round: the keys are still in registers
+      load_round(rr);
+      score_round();
+    }
+    if (mine) {
+#pragma unroll
+      for (int u = 0; u < kSampleSlots; ++u)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t kk = key[u][x];
+          if (kk == 0u) continue;
+          const int j = hsel + (x & 1);
+          const int b1 = (int)(kk >> kSampleSh1);
+          const uint32_t b2 = (kk >> kSampleSh2) & 255u;
+          if (b1 == ((x & 1) ? bl1 : bl0)) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
+          if (b1 == ((x & 1) ? bh1 : bh0)) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+        }
+    }
+  }
+  __syncthreads();
+  if (warp < 2 * H) {
+    const int j = warp >> 1, e = warp & 1;
+    int bin;
+    uint32_t res;
+    warp_find_bin256(hist2 + (j * 2 + e) * 256, s_res[j][e], &bin, &res);
+    if (lane == 0) {
+      const uint32_t pre = ((uint32_t)s_bin1[j][e] << kSampleSh1) | ((uint32_t)bin << kSampleSh2);
+      s_lohi[j][e] = e ? (pre | ((1u << kSampleSh2) - 1u)) : pre;  // hi: bin ceiling, lo: bin floor
+    }
+  }
+  __syncthreads();
+  if (tid < H) {
+    uint32_t lo = s_lohi[tid][0], hi = s_lohi[tid][1];
+    if (r_lo > n_s) lo = 0u;         // not enough sample mass: every token is a candidate
+    if (r_hi < 1) hi = 0xFFFFFFFFu;  // no token is sure
+    const size_t row = (size_t)row0 + j0 + tid;
+    const float flo = thresh_lo(lo), fsure = hi == 0xFFFFFFFFu ? INFINITY : thresh_lo(hi + 1u);
+    reinterpret_cast<uint4*>(thr)[row] = make_uint4(lo, hi, __float_as_uint(flo), __float_as_uint(fsure));
+  }
+}
+
 // --------------------------------------------------------------------------- select core (kernel 3.)
 // Arguments of the select step (the kernel parameter of sbs_select_kernel).
 struct SelArgs {
@@ -1318,10 +1517,24 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     const size_t smem_used = split ? sizeof(uint32_t) * GH * (kHistWords + 512) + sizeof(float) * GH * C + (size_t)GH * kD * 4 +
                                          sizeof(int) * C + sizeof(uint32_t) * GH * 32
                                    : smem;
-    e = set_smem(kern, smem_used);
-    if (e != cudaSuccess) return e;
-    e = launch_pdl(kern, dim3(split ? 2 * BG : BG), dim3(snt), smem_used, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
-                   kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
+    if (SkMma<G, Sk>::value && C == 8) {  // tensor-core sample (the scan's scores)
+      const int H = split ? 2 : 4;
+      const size_t smem_m = sizeof(uint32_t) * H * (kHistWords + 512) + (size_t)4 * kD * 4 + sizeof(int) * 8 +
+                            sizeof(uint32_t) * H * 32;
+      auto km = snt == 512 ? sbs_sample_mma_kernel<512, 4, false>
+                : split ? (multi ? sbs_sample_mma_kernel<kSampleThreads, 2, true> : sbs_sample_mma_kernel<kSampleThreads, 2, false>)
+                        : (multi ? sbs_sample_mma_kernel<kSampleThreads, 4, true> : sbs_sample_mma_kernel<kSampleThreads, 4, false>);
+      e = set_smem(km, smem_m);
+      if (e != cudaSuccess) return e;
+      e = launch_pdl(km, dim3(split ? 2 * BG : BG), dim3(snt), smem_m, st, false, q, geo.kv_dtype,
+                     reinterpret_cast<const uint16_t*>(sk), skc.channel_ids, kv.page_table, kv.seq_lens, geo.max_seq_len,
+                     geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
+    } else {
+      e = set_smem(kern, smem_used);
+      if (e != cudaSuccess) return e;
+      e = launch_pdl(kern, dim3(split ? 2 * BG : BG), dim3(snt), smem_used, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
+                     kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
+    }
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[0], st);
   }
