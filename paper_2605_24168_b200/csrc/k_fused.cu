@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_kernel(
   __syncthreads();
   if (N < 1) return;
   const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
-  const int k = min(rbud.k, N);
+  const int k = bud.kfrom ? max(0, shard_row_k(bud, b, N)) : min(rbud.k, N);
   uint32_t key[kSampleSlots][G];
   auto score_round = [&]() {
 #pragma unroll
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_mma_kernel(
       },
       q_dtype == SD_F32 ? 3 : 1);
   const RowBudget rbud = row_budget(N, bud);  // NEXT-1: sinks / locals score +inf
-  const int k = min(rbud.k, N);
+  const int k = bud.kfrom ? max(0, shard_row_k(bud, b, N)) : min(rbud.k, N);
   const int last_sampled = (ns_pages - 1) * spg;
   const int n_s = ns_pages * 16 - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
   int r_lo, r_hi;
@@ -715,7 +715,11 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
   }
   pdl_wait();
   const RowBudget rb = row_budget(max(N, 0), bud);
-  const int k = N >= 1 ? rb.k : 0;
+  const int k = bud.kfrom ? (N >= 0 ? shard_row_k(bud, b, N) : -1) : (N >= 1 ? rb.k : 0);
+  if (bud.kfrom && N == 0 && k == 0) {  // an empty shard of a valid sequence: no candidates
+    if (counts_out && tid < HPC) counts_out[row_base + tid] = 0;
+    return;
+  }
   if (N < 1 || k > N || (k < 1 && !budget_regions(bud))) {
     if (tid < HPC) {
       set_error(err, SD_DEVERR_SEQLEN);
@@ -1453,6 +1457,134 @@ __global__ void __launch_bounds__(kIdxNT) sbs_idx_kernel(const int* __restrict__
   }
 }
 
+// --------------------------------------------------------------------------- 5. shard candidates
+// Sequence shard: the selection bitmap of every q-row
+// of (b, g) -> its candidates in ascending local index order with their fp32
+// indexer scores (cand_idx / cand_scores [B*Hq][k_max], -1 / -inf padded).
+// G = 4, C = 8, bf16 sketch: a selected token's score is recomputed with the
+// scan's MMA on the same 32-token block, so it is the scan's bits.  Grid
+// (8192-token tiles, B*Hkv); a tile's output offset per head = the set bits of
+// the head's earlier tiles.
+constexpr int kEmitNT = 256;
+__global__ void __launch_bounds__(kEmitNT) sbs_emit_kernel(
+    const void* __restrict__ q, int q_dtype, const uint16_t* __restrict__ sk, const int* __restrict__ channel_ids,
+    const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
+    const uint32_t* __restrict__ fbm, int ldw, const int* __restrict__ counts, int* __restrict__ cand_idx,
+    float* __restrict__ cand_scores, int k_max) {
+  constexpr int G = 4, C = 8, kW = kRangeTok / 32;  // words per tile and head
+  static_assert(kW == kEmitNT, "one selection word per thread and head");
+  __shared__ uint32_t s_w[G][kW];
+  __shared__ int s_pre[G][kW];
+  __shared__ int s_wt[G][kEmitNT / 32];
+  __shared__ int s_base[G];
+  __shared__ float s_qc[G * C];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
+  const int Hq = Hkv * G, row0 = b * Hq + g * G;
+  const int tile = blockIdx.x, T0 = tile * kRangeTok;
+  pdl_wait();  // the bitmaps and counts come from the select
+  const int N = max(0, seq_len_dev(seq_lens, b, max_len));
+  if (tile == 0) {  // padding past each row's count
+    for (int j = 0; j < G; ++j) {
+      const int c = max(0, counts[row0 + j]);
+      for (int i = c + tid; i < k_max; i += kEmitNT) {
+        cand_idx[(size_t)(row0 + j) * k_max + i] = -1;
+        cand_scores[(size_t)(row0 + j) * k_max + i] = -INFINITY;
+      }
+    }
+  }
+  if (T0 >= N) return;
+  const int nwt = min(kW, (N - T0 + 31) >> 5);
+  if (tid < G * C) {
+    const int j = tid / C, c = tid - j * C;
+    const int ch = __ldg(channel_ids + (size_t)bg * C + c);
+    const size_t e = (size_t)(row0 + j) * kD + ch;
+    s_qc[tid] = q_dtype == SD_F32 ? reinterpret_cast<const float*>(q)[e] : bf_lo(reinterpret_cast<const uint16_t*>(q)[e]);
+  }
+  // set bits of the earlier tiles, per head
+  int before[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    int c = 0;
+    const uint32_t* fr = fbm + (size_t)(row0 + j) * ldw;
+    for (int w = tid; w < tile * kW; w += kEmitNT) c += __popc(fr[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    before[j] = c;
+  }
+  // this tile's words and their exclusive prefix per head
+  int incl[G], cnt[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const uint32_t w = tid < nwt ? fbm[(size_t)(row0 + j) * ldw + (T0 >> 5) + tid] : 0u;
+    s_w[j][tid] = w;
+    cnt[j] = __popc(w);
+    incl[j] = cnt[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl[j], o);
+      if (lane >= o) incl[j] += y;
+    }
+    if (lane == 31) s_wt[j][warp] = incl[j];
+  }
+  __shared__ int s_before[G][kEmitNT / 32];
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) s_before[j][warp] = before[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    int wb = 0;
+    for (int w = 0; w < warp; ++w) wb += s_wt[j][w];
+    s_pre[j][tid] = wb + incl[j] - cnt[j];
+  }
+  if (tid < G) {
+    int bb = 0;
+    for (int w = 0; w < kEmitNT / 32; ++w) bb += s_before[tid][w];
+    s_base[tid] = bb;
+  }
+  __syncthreads();
+  const SkMmaQ qm = sk_mma_q([](int j, int c) { return s_qc[j * C + c]; }, q_dtype == SD_F32 ? 3 : 1);
+  const int* pt = page_table + (size_t)b * max_pages;
+  const int r = lane >> 2, uu = lane & 3, h0 = 2 * (uu & 1);
+  const int tofs = r + ((uu >> 1) << 4);
+  // warp per 32-token block (selection word), 4 blocks in flight
+  for (int i0 = warp; i0 < nwt; i0 += 4 * (kEmitNT / 32)) {
+    uint32_t a[4][4];
+    bool any[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int wi = i0 + u * (kEmitNT / 32);
+      any[u] = wi < nwt && (s_w[0][wi] | s_w[1][wi] | s_w[2][wi] | s_w[3][wi]) != 0u;
+      if (any[u]) {
+        const int t0 = T0 + wi * 32;
+        sk_mma_a_global(a[u], sk, t0, N,
+                        [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C); });
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!any[u]) continue;
+      const int wi = i0 + u * (kEmitNT / 32);
+      float d[4];
+      sk_mma_score(a[u], qm, d);
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int j = h0 + (x & 1), bit = tofs + 8 * (x >> 1);
+        const uint32_t w = s_w[j][wi];
+        if ((w >> bit) & 1u) {
+          const int pos = s_base[j] + s_pre[j][wi] + __popc(w & ((1u << bit) - 1u));
+          if (pos < k_max) {
+            cand_idx[(size_t)(row0 + j) * k_max + pos] = T0 + wi * 32 + bit;
+            cand_scores[(size_t)(row0 + j) * k_max + pos] = d[x];
+          }
+        }
+      }
+    }
+  }
+}
+
 template <class Kern>
 cudaError_t set_smem(Kern k, size_t bytes) {
   return ensure_dyn_smem(reinterpret_cast<const void*>(k), bytes);
@@ -1480,9 +1612,10 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 // the low end, 1 at the high end).
 int band_capacity(int max_seq_len, Budget bud, int sample_nt) {
   const double N = std::max(1, max_seq_len);
-  const double k = bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, N)
-                   : bud.regions() ? std::max(1.0, bud.heavy_fraction * N + bud.n_sink + bud.n_local)
-                                   : std::ceil(N / bud.S);
+  const double NK = bud.kfrom ? std::max(1, bud.max_from) : N;  // sequence shard: k_b from the global length
+  const double k = std::min(N, bud.k_fixed > 0 ? std::min<double>(bud.k_fixed, NK)
+                               : bud.regions() ? std::max(1.0, bud.heavy_fraction * N + bud.n_sink + bud.n_local)
+                                               : std::ceil(NK / bud.S));
   const double f = std::min(1.0, (double)sample_rounds(max_seq_len) * sample_nt * kSampleSlots / N);
   const double sig = std::sqrt(k * f * (1.0 - f));
   // the band spans dr sample ranks; the tokens between two sample order
@@ -1580,6 +1713,16 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
 }
 
 }  // namespace
+
+cudaError_t launch_sbs_emit(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
+                            const SbsBuffers& w, int* cand_idx, float* cand_scores, int k_max, cudaStream_t st) {
+  if (g.G != 4 || sk.channels != 8 || sk.dtype != SD_BF16) return cudaErrorInvalidValue;
+  const int nch = (g.max_seq_len + kRangeTok - 1) / kRangeTok;
+  return launch_pdl(sbs_emit_kernel, dim3(nch, g.B * g.Hkv), dim3(kEmitNT), 0, st, true, q, g.kv_dtype,
+                    reinterpret_cast<const uint16_t*>(sk.pages), sk.channel_ids, kv.page_table, kv.seq_lens,
+                    g.max_seq_len, g.max_pages, g.Hkv, (const uint32_t*)w.fbm, w.ldw, (const int*)w.counts_out,
+                    cand_idx, cand_scores, k_max);
+}
 
 cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q, Budget bud,
                               const SbsBuffers& w, cudaStream_t st) {

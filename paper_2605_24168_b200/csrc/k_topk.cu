@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
 __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
     const float* __restrict__ all_cand, const int* __restrict__ cand_idx, int parts, int rank,
     int rows, int Hq, const int* __restrict__ global_seq_lens, double S, int k_fixed, int k_max,
-    int* __restrict__ surv, int* __restrict__ surv_cnt, int* __restrict__ err) {
+    int* __restrict__ surv, int* __restrict__ surv_cnt, int* __restrict__ err, uint32_t* __restrict__ fbm, int ldw,
+    int nw_local) {
   __shared__ SelectSmem<kTkThreads> sm;
   __shared__ uint32_t s_eq_before;
   const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
@@ -86,6 +87,10 @@ __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
     if (tid == 0) { set_error(err, SD_DEVERR_SEQLEN); surv_cnt[row] = 0; }
     return;
   }
+  // fbm (optional): the survivors as this rank's selection bitmap row (local tokens)
+  uint32_t* fr = fbm ? fbm + (size_t)row * ldw : nullptr;
+  if (fr)
+    for (int w = tid; w < nw_local; w += kTkThreads) fr[w] = 0u;  // ordered before the bits by the select's barriers
   const int n = parts * k_max;
   auto key_all = [=](int i) {
     const int p = i / k_max, j = i - p * k_max;
@@ -106,8 +111,10 @@ __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
   int* out = surv + (size_t)row * k_max;
   auto key_mine = [mine](int i) { return score_key(__ldg(mine + i)); };
   const uint32_t c = emit_block<kTkThreads, 4>(key_mine, k_max, tau, need_eq, eq_before, sm,
-                                               [out, mid](uint32_t pos, int i, uint32_t) {
-                                                 out[pos] = __ldg(mid + i);
+                                               [out, mid, fr](uint32_t pos, int i, uint32_t) {
+                                                 const int t = __ldg(mid + i);
+                                                 out[pos] = t;
+                                                 if (fr) atomicOr(fr + (t >> 5), 1u << (t & 31));
                                                });
   if (tid == 0) surv_cnt[row] = (int)c;
 }
@@ -133,10 +140,10 @@ cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const i
 
 cudaError_t launch_seqshard_cut(const Geo& g, const float* all_cand, const int* cand_idx, int parts,
                                 int rank, const int* global_lens, Budget bud, int k_max, int* surv,
-                                int* surv_cnt, int* err, cudaStream_t st) {
+                                int* surv_cnt, int* err, cudaStream_t st, uint32_t* fbm, int ldw) {
   seqshard_cut_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(all_cand, cand_idx, parts, rank, g.B * g.Hq,
                                                          g.Hq, global_lens, bud.S, bud.k_fixed, k_max,
-                                                         surv, surv_cnt, err);
+                                                         surv, surv_cnt, err, fbm, ldw, (g.max_seq_len + 31) / 32);
   return cudaGetLastError();
 }
 

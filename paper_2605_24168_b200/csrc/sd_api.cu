@@ -329,6 +329,25 @@ sd_status sd_sparse_gather_attend(const sd_geometry* geom, const sd_paged_kv* kv
 
 namespace {
 
+SbsBuffers sbs_buffers(void* ws, const WsLayout& L) {
+  SbsBuffers w;
+  w.thr = reinterpret_cast<uint32_t*>(wsp(ws, L.thr));
+  w.ent_tok = reinterpret_cast<uint32_t*>(wsp(ws, L.ent_tok));
+  w.ent_sc = reinterpret_cast<float*>(wsp(ws, L.ent_sc));
+  w.ent_cnt = reinterpret_cast<int*>(wsp(ws, L.ent_cnt));
+  w.fbm = reinterpret_cast<uint32_t*>(wsp(ws, L.fbm));
+  w.counters = reinterpret_cast<int*>(wsp(ws, L.ctr));
+  w.ldw = L.ldw;
+  w.scratch = reinterpret_cast<float*>(wsp(ws, L.scores));
+  w.ld = L.ld;
+  w.counts_out = nullptr;
+  w.idx_out = nullptr;
+  w.k_max_out = 0;
+  w.force_fallback = 0;
+  w.err = reinterpret_cast<int*>(ws);
+  return w;
+}
+
 // The fused step; ev (nullable) = 6 events: [0] before the first kernel, then
 // one after each of sample, scan, select, attend, merge (bf16 sketch path).
 sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sketch* sketch, const void* q,
@@ -363,16 +382,7 @@ sd_status fused_impl(const sd_geometry* geom, const sd_paged_kv* kv, const sd_sk
     return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));
   }
   // sketch (Double Sparsity) mode: sample-bracket select, scores stay on chip
-  SbsBuffers w;
-  w.thr = reinterpret_cast<uint32_t*>(wsp(ws, L.thr));
-  w.ent_tok = reinterpret_cast<uint32_t*>(wsp(ws, L.ent_tok));
-  w.ent_sc = reinterpret_cast<float*>(wsp(ws, L.ent_sc));
-  w.ent_cnt = reinterpret_cast<int*>(wsp(ws, L.ent_cnt));
-  w.fbm = reinterpret_cast<uint32_t*>(wsp(ws, L.fbm));
-  w.counters = reinterpret_cast<int*>(wsp(ws, L.ctr));
-  w.ldw = L.ldw;
-  w.scratch = reinterpret_cast<float*>(wsp(ws, L.scores));
-  w.ld = L.ld;
+  SbsBuffers w = sbs_buffers(ws, L);
   w.counts_out = counts_out;
   w.idx_out = idx_out;
   w.k_max_out = idx_out ? k_max_out : 0;
@@ -485,7 +495,17 @@ sd_status sd_seqshard_local_topk(const sd_geometry* geom, const sd_paged_kv* kv,
   int* err = reinterpret_cast<int*>(ws);
   float* scores = reinterpret_cast<float*>(wsp(ws, L.scores));
   int* counts = reinterpret_cast<int*>(wsp(ws, L.counts));
-  const Budget bud = to_budget(budget);
+  Budget bud = to_budget(budget);
+  if (sketch && g.G == 4 && sketch->channels == 8 && sketch->dtype == SD_BF16) {
+    // the fused selection with k_b from the global lengths (scores stay on chip),
+    // then the candidates and their scores from the selection bitmaps
+    bud.kfrom = global_seq_lens;
+    bud.max_from = max_global_seq_len;
+    SbsBuffers w = sbs_buffers(ws, L);
+    w.counts_out = counts;
+    SD_CUDA(launch_sbs_select(g, *kv, *sketch, q, bud, w, st));
+    return cuda_status(launch_sbs_emit(g, *kv, *sketch, q, w, cand_idx, cand_scores, k_max, st));
+  }
   SD_CUDA(launch_index_score(g, *kv, sketch, q, scores, L.ld, st));
   return cuda_status(launch_topk_shard(g, scores, L.ld, kv->seq_lens, global_seq_lens, max_global_seq_len, bud, cand_idx,
                                        counts, cand_scores, k_max, err, st));
@@ -513,11 +533,24 @@ sd_status sd_seqshard_cut_attend(const sd_geometry* geom, const sd_paged_kv* kv,
   int* surv = surv_idx ? surv_idx : reinterpret_cast<int*>(wsp(ws, L.idx));
   int* surv_cnt = surv_counts ? surv_counts : reinterpret_cast<int*>(wsp(ws, L.counts));
   const Budget bud = to_budget(budget);
+  const int rows = g.B * g.Hq;
+  float* part = reinterpret_cast<float*>(wsp(ws, L.part));
+  if (g.kv_dtype == SD_BF16) {
+    // survivors -> selection bitmap rows -> the GQA-union gather-attend (each
+    // K/V row fetched once per group) -> normalised (o, lse) per row
+    uint32_t* fbm = reinterpret_cast<uint32_t*>(wsp(ws, L.fbm));
+    int* ctr = reinterpret_cast<int*>(wsp(ws, L.ctr));
+    SD_CUDA(launch_seqshard_cut(g, all_cand, cand_idx, parts, rank, global_seq_lens, bud, k_max, surv, surv_cnt,
+                                err, st, fbm, L.ldw));
+    SD_CUDA(cudaMemsetAsync(ctr + g.B * g.Hkv, 0, sizeof(int), st));  // the attend's work counter
+    Geo gf = g;
+    gf.out_dtype = SD_F32;
+    return cuda_status(launch_attend_union_pk(gf, *kv, q, fbm, L.ldw, scale, part, part_o, part_lse, ctr, st,
+                                              nullptr));
+  }
   SD_CUDA(launch_seqshard_cut(g, all_cand, cand_idx, parts, rank, global_seq_lens, bud, k_max, surv,
                               surv_cnt, err, st));
-  const int rows = g.B * g.Hq;
   const int splits = choose_splits(rows, k_max, 64);
-  float* part = reinterpret_cast<float*>(wsp(ws, L.part));
   SD_CUDA(launch_attend_list(g, *kv, q, surv, surv_cnt, k_max, nullptr, scale, part, splits, 1, err, st));
   // normalised (o, lse) per row for the cross-rank merge
   SD_CUDA(launch_merge_parts(part, rows, splits, part_o, SD_F32, part_lse, st));

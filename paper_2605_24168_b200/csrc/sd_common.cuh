@@ -56,6 +56,10 @@ struct BudgetDev {
   double S;
   int k_fixed, n_sink, n_local;
   double heavy_fraction;
+  // sequence shard: k_b from the sequence's GLOBAL length
+  // kfrom[b] (<= max_from), at most the local N_b; null: from the local N_b
+  const int* kfrom = nullptr;
+  int max_from = 0;
 };
 struct RowBudget {
   int lo, hi, k;  // middle region [lo, hi), total selected k (0 allowed in NEXT-1 mode)
@@ -79,6 +83,12 @@ __device__ __forceinline__ RowBudget row_budget(int N, const BudgetDev& b) {
   else kh = min(mid, (int)floor(b.heavy_fraction * (double)mid + 0.5));
   r.k = r.lo + (N - r.hi) + kh;
   return r;
+}
+
+// k_b of a sequence shard: from the global length, at most the local N (-1: invalid global length).
+__device__ __forceinline__ int shard_row_k(const BudgetDev& b, int bi, int N) {
+  const int NG = seq_len_dev(b.kfrom, bi, b.max_from);
+  return NG >= 1 ? min(budget_k_dev(NG, b.S, b.k_fixed), max(N, 0)) : -1;
 }
 
 // ---------------------------------------------------------------- radix keys

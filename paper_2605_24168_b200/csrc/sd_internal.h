@@ -35,7 +35,9 @@ struct Budget {
   int k_fixed;
   int n_sink = 0, n_local = 0;
   double heavy_fraction = 0.0;
-  BudgetDev dev() const { return BudgetDev{S, k_fixed, n_sink, n_local, heavy_fraction}; }
+  const int* kfrom = nullptr;  // sequence shard: k_b from these global lengths (<= max_from)
+  int max_from = 0;
+  BudgetDev dev() const { return BudgetDev{S, k_fixed, n_sink, n_local, heavy_fraction, kfrom, max_from}; }
   bool regions() const { return n_sink != 0 || n_local != 0 || heavy_fraction != 0.0; }
 };
 
@@ -80,9 +82,10 @@ cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const i
                               const int* global_lens, int max_global, Budget bud, int* idx, int* counts,
                               float* cand_scores, int k_max, int* err, cudaStream_t st);
 
+// fbm (nullable): also write the survivors as selection bitmap rows [B*Hq][ldw] over the local tokens
 cudaError_t launch_seqshard_cut(const Geo& g, const float* all_cand, const int* cand_idx, int parts,
                                 int rank, const int* global_lens, Budget bud, int k_max, int* surv,
-                                int* surv_cnt, int* err, cudaStream_t st);
+                                int* surv_cnt, int* err, cudaStream_t st, uint32_t* fbm = nullptr, int ldw = 0);
 
 // Combine `splits` unnormalised partials per row into out / lse.
 cudaError_t launch_merge_parts(const float* part, int rows, int splits, void* out,
@@ -124,6 +127,10 @@ struct SbsBuffers {
 
 cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
                               Budget bud, const SbsBuffers& w, cudaStream_t st);
+// sequence shard: selection bitmaps (after launch_sbs_select with bud.kfrom) -> ascending
+// candidates + their fp32 scores (G = 4, C = 8, bf16 sketch only)
+cudaError_t launch_sbs_emit(const Geo& g, const sd_paged_kv& kv, const sd_sketch& sk, const void* q,
+                            const SbsBuffers& w, int* cand_idx, float* cand_scores, int k_max, cudaStream_t st);
 
 // ---- row-list gather-attend (k_rows.cu: fp32 KV on the CUDA cores; k_rows_mma.cu: bf16 dense decode on the tensor cores)
 cudaError_t launch_attend_rows(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,

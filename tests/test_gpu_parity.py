@@ -696,6 +696,38 @@ def test_seqshard_protocol_matches_oracle(cuda_lib, P, dist):
             check_lse(lse[b, h], rl)
 
 
+@pytest.mark.parametrize("dist", ["needle", "dup"])
+def test_seqshard_local_candidates_exact(cuda_lib, dist):
+    """Sequence-shard step 1 on the fused selection (k_b from the GLOBAL length,
+    scores never materialised): every shard's candidates are exactly the
+    top-min(k_b, N_loc) of the GPU's own fp32 indexer scores of the shard
+    (ties to the lower index), ascending, with those scores bit for bit, padded
+    with -1 / -inf; shards past a short sequence's end are empty."""
+    sd = cuda_lib
+    lens = [8192 + 5, 3000]
+    case = _dev(workloads.make_case(2, 32, 8, lens, seed=71, dist=dist, n_needles=60))
+    _, sk = _kv(sd, case)
+    S, P, NG = 20.0, 3, max(lens)
+    glens = case.seq_lens
+    k_max = sd.budget_k(S, NG)
+    bounds = [((r * NG) // P) // 16 * 16 for r in range(P)] + [NG]
+    for r in range(P):
+        kvr, loc = _shard_kv(sd, case, bounds[r], bounds[r + 1])
+        sd.clear_device_error()
+        cs, ci = sd.seqshard_local_topk(case.q, kvr, sk, glens, NG, S, k_max=k_max)
+        sc = sd.sparse_index_score(case.q, kvr, sk)
+        assert sd.read_device_error() == 0
+        cs, ci, sc = cs.cpu().numpy(), ci.cpu().numpy(), sc.cpu().numpy()
+        for b in range(2):
+            nl = int(loc[b])
+            k = min(sd.budget_k(S, lens[b]), nl)
+            for h in range(32):
+                exp = oracle.topk_select(sc[b, h, :nl].astype(np.float64), k) if k else np.zeros(0, np.int64)
+                assert np.array_equal(ci[b, h, :k], exp), (r, b, h)
+                assert np.array_equal(cs[b, h, :k].view(np.uint32), sc[b, h, exp].view(np.uint32))
+                assert np.all(ci[b, h, k:] == -1) and np.all(np.isneginf(cs[b, h, k:]))
+
+
 @pytest.mark.parametrize("dist", ["iid", "needle", "dup"])
 def test_fused_forced_fallback_identical(cuda_lib, dist):
     """The exact per-(b, g) fallback of the fused select (sd_sparse_decode_fused_ex
