@@ -520,7 +520,57 @@ cudaError_t launch_pk_t(const Geo& g, const sd_paged_kv& kv, const void* q, cons
   return launch_merge_parts_pdl(part, g.B * g.Hq, splits, out, g.out_dtype, lse, st);
 }
 
+// Index lists -> selection bitmap rows (sd_sparse_gather_attend's union path).
+// One CTA per q-row; rows up to kI2bWords * 32 tokens are assembled in shared
+// memory and stored word by word, longer rows are zeroed and set in place.
+constexpr int kI2bNT = 256;
+constexpr int kI2bWords = 8192;
+__global__ void __launch_bounds__(kI2bNT) idx_to_bits_kernel(const int* __restrict__ idx,
+                                                             const int* __restrict__ counts, int k_max,
+                                                             const int* __restrict__ seq_lens, int max_len, int Hq,
+                                                             uint32_t* __restrict__ fbm, int ldw, int* __restrict__ work,
+                                                             int* __restrict__ err) {
+  __shared__ uint32_t sw[kI2bWords];
+  const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
+  if (row == 0 && tid == 0) *work = 0;
+  const int N = seq_len_dev(seq_lens, b, max_len);  // -1 (out of range): every count is rejected
+  int cnt = __ldg(counts + row);
+  if (cnt < 1 || cnt > k_max || cnt > N) {
+    if (tid == 0) set_error(err, cnt < 1 ? SD_DEVERR_EMPTY : SD_DEVERR_SEQLEN);
+    cnt = max(0, min(cnt, min(k_max, max(N, 0))));
+  }
+  const int nw = (max(N, 0) + 31) >> 5;
+  uint32_t* fr = fbm + (size_t)row * ldw;
+  const bool in_smem = nw <= kI2bWords;
+  uint32_t* tw = in_smem ? sw : fr;
+  for (int w = tid; w < nw; w += kI2bNT) tw[w] = 0u;
+  __syncthreads();
+  const int* ip = idx + (size_t)row * k_max;
+  for (int e = tid; e < cnt; e += kI2bNT) {
+    const int t = __ldg(ip + e);
+    bool ok = t >= 0 && t < N;
+    if (ok && e > 0 && __ldg(ip + e - 1) >= t) {
+      ok = false;
+      set_error(err, SD_DEVERR_INDEX_ORDER);
+    } else if (!ok) {
+      set_error(err, SD_DEVERR_INDEX_RANGE);
+    }
+    if (ok) atomicOr(tw + (t >> 5), 1u << (t & 31));
+  }
+  if (in_smem) {
+    __syncthreads();
+    for (int w = tid; w < nw; w += kI2bNT) fr[w] = sw[w];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_idx_to_bits(const Geo& g, const int* seq_lens, const int* idx, const int* counts, int k_max,
+                               uint32_t* fbm, int ldw, int* work, int* err, cudaStream_t st) {
+  idx_to_bits_kernel<<<g.B * g.Hq, kI2bNT, 0, st>>>(idx, counts, k_max, seq_lens, g.max_seq_len, g.Hq, fbm, ldw,
+                                                    work, err);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_attend_union_pk(const Geo& g, const sd_paged_kv& kv, const void* q, const uint32_t* fbm, int ldw,
                                    float scale, float* part, void* out, float* lse, int* counters, cudaStream_t st,

@@ -167,12 +167,12 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, 
   a1 = __uint_as_float((uint32_t)(r >> 32));
 }
 
-// Predicated candidate store (no branch): {x, y} -> *c2, code -> *ct when p.
-__device__ __forceinline__ void st_cand_pred(bool p, float2* c2, float x, float y, uint16_t* ct, uint16_t code) {
+// Predicated candidate store (no branch): {x, y} -> shared [a2], code -> shared [at] when p.
+__device__ __forceinline__ void st_cand_pred(bool p, uint32_t a2, float x, float y, uint32_t at, uint16_t code) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
       "@q st.shared.v2.f32 [%1], {%2, %3};\n\t@q st.shared.u16 [%4], %5;\n}" ::"r"((int)p),
-      "r"(smem_u32(c2)), "f"(x), "f"(y), "r"(smem_u32(ct)), "h"(code)
+      "r"(a2), "f"(x), "f"(y), "r"(at), "h"(code)
       : "memory");
 }
 
@@ -1208,6 +1208,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const float pm_fl0 = pm_p ? pm_flb0 : pm_fla0, pm_fl1 = pm_p ? pm_flb1 : pm_fla1;
   float2* pm_c2 = reinterpret_cast<float2*>(c_sc_all) + warp * 2 * kScanCandCap;  // [2 * kScanCandCap]
   uint16_t* pm_ct = c_tok_all + warp * 2 * kScanCandCap;
+  const uint32_t pm_c2_s = smem_u32(pm_c2), pm_ct_s = smem_u32(pm_ct);  // shared-window addresses
 
   // ---- phase 2: classify the buffered candidates, one per lane: sure bits into
   // the chunk's words (shared-memory atomics), band tokens into the region
@@ -1327,8 +1328,10 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
             const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
             const int nA = __popc(bA);
             const int pA = wn + __popc(bA & lt_mask), pB = wn + nA + __popc(bB & lt_mask);
-            st_cand_pred(cA, pm_c2 + pA, d[h][0], d[h][1], pm_ct + pA, (uint16_t)((cb + tA) | (pm_p << 15)));
-            st_cand_pred(cB, pm_c2 + pB, d[h][2], d[h][3], pm_ct + pB, (uint16_t)((cb + tB) | (pm_p << 15)));
+            st_cand_pred(cA, pm_c2_s + 8u * (uint32_t)pA, d[h][0], d[h][1], pm_ct_s + 2u * (uint32_t)pA,
+                         (uint16_t)((cb + tA) | (pm_p << 15)));
+            st_cand_pred(cB, pm_c2_s + 8u * (uint32_t)pB, d[h][2], d[h][3], pm_ct_s + 2u * (uint32_t)pB,
+                         (uint16_t)((cb + tB) | (pm_p << 15)));
             wn += nA + __popc(bB);
           }
         }

@@ -36,7 +36,8 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
   size_t off = 256;  // error word + reserved
   const size_t rows = (size_t)B * Hq;
   if (with_budget) L.nrange = (max_seq_len + kRangeTok - 1) / kRangeTok;
-  L.part_splits = std::max(kMaxSplits, L.nrange);
+  // split partials: the list / dense paths use <= kMaxSplits, the GQA-union attend one per 8192-token range
+  L.part_splits = std::max(kMaxSplits, (max_seq_len + kRangeTok - 1) / kRangeTok);
   L.part = off;
   off = align256(off + rows * (size_t)L.part_splits * kPartStride * sizeof(float));
   L.ctr = off;
@@ -63,6 +64,12 @@ WsLayout ws_layout(int B, int Hq, int Hkv, int max_seq_len, bool with_budget, in
     off = align256(off + nreg * cap * G * sizeof(float));
     L.ent_cnt = off;
     off = align256(off + nreg * nsub * sizeof(int));
+    L.fbm = off;
+    off = align256(off + rows * (size_t)L.ldw * sizeof(uint32_t));
+  } else {
+    // selection bitmaps for sd_sparse_gather_attend's GQA-union path
+    L.ld = (max_seq_len + 63) & ~63;
+    L.ldw = L.ld / 32;
     L.fbm = off;
     off = align256(off + rows * (size_t)L.ldw * sizeof(uint32_t));
   }
@@ -319,9 +326,19 @@ sd_status sd_sparse_gather_attend(const sd_geometry* geom, const sd_paged_kv* kv
   const WsLayout L = ws_layout(g.B, g.Hq, g.Hkv, kv->max_seq_len, false, 0);
   SD_TRY(check_ws(ws, ws_bytes, L.total));
   const int rows = g.B * g.Hq;
-  const int splits = choose_splits(rows, k_max, 64);
   float* part = reinterpret_cast<float*>(wsp(ws, L.part));
   cudaStream_t st = (cudaStream_t)stream;
+  if (!weights && g.kv_dtype == SD_BF16) {
+    // unit weights, bf16 KV: the index lists -> selection bitmaps (same per-entry
+    // checks) -> the GQA-union gather-attend: a K/V row selected by several
+    // q-heads of a group is fetched once, scored on the tensor cores
+    uint32_t* fbm = reinterpret_cast<uint32_t*>(wsp(ws, L.fbm));
+    int* ctr = reinterpret_cast<int*>(wsp(ws, L.ctr));
+    SD_CUDA(launch_idx_to_bits(g, kv->seq_lens, idx, counts, k_max, fbm, L.ldw, ctr + g.B * g.Hkv,
+                               reinterpret_cast<int*>(ws), st));
+    return cuda_status(launch_attend_union_pk(g, *kv, q, fbm, L.ldw, scale, part, out, lse, ctr, st, nullptr));
+  }
+  const int splits = choose_splits(rows, k_max, 64);
   SD_CUDA(launch_attend_list(g, *kv, q, idx, counts, k_max, weights, scale, part, splits, 0,
                              reinterpret_cast<int*>(ws), st));
   return cuda_status(launch_merge_parts(part, rows, splits, out, g.out_dtype, lse, st));

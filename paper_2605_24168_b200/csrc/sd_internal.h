@@ -15,8 +15,10 @@ constexpr int kPageSize = 16;       // the only compiled page size
 constexpr int kMaxSplits = 64;      // split-k partial slots per (b, h) row (dense / list paths)
 constexpr int kPartStride = 128 + 2;  // {m (log2 domain), l, o[128] unnormalised}
 constexpr int kScanWarps = 8;         // warps per scan CTA = band regions per 8192-token range
-// union-band entries per (b, g, region of 1024 tokens): 128 per q-head of the group
-constexpr int band_region_cap(int G) { return G >= 8 ? 1024 : 128 * G; }
+// union-band entries per (b, g, region of 1024 tokens): 512 per head pair (G = 4, the
+// tensor-core scan's pair regions), 128 per q-head + 128 for G <= 2 (S = 2 puts ~10% of
+// a head's tokens in the band: 95-135 per region at G = 1, measured), every token at G = 8
+constexpr int band_region_cap(int G) { return G >= 8 ? 1024 : G == 4 ? 512 : 128 * G + 128; }
 
 // Resolved, validated arguments passed from the C-ABI layer to launchers.
 struct Geo {
@@ -82,6 +84,12 @@ cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const i
                               const int* global_lens, int max_global, Budget bud, int* idx, int* counts,
                               float* cand_scores, int k_max, int* err, cudaStream_t st);
 
+// Per-head index lists (ascending, < N_b; checked per entry like attend_list_kernel: an
+// out-of-range / out-of-order entry is skipped with SD_DEVERR_INDEX_RANGE / _ORDER, a count
+// outside [1, min(k_max, N_b)] clamped with SD_DEVERR_EMPTY / _SEQLEN) -> selection bitmap
+// rows fbm [B*Hq][ldw]; also zeroes *work (the GQA-union attend's item counter).
+cudaError_t launch_idx_to_bits(const Geo& g, const int* seq_lens, const int* idx, const int* counts, int k_max,
+                               uint32_t* fbm, int ldw, int* work, int* err, cudaStream_t st);
 // fbm (nullable): also write the survivors as selection bitmap rows [B*Hq][ldw] over the local tokens
 cudaError_t launch_seqshard_cut(const Geo& g, const float* all_cand, const int* cand_idx, int parts,
                                 int rank, const int* global_lens, Budget bud, int k_max, int* surv,

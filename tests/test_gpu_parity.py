@@ -193,6 +193,36 @@ def test_gather_attend_matches_oracle(cuda_lib, dtype, out_dtype, weighted):
             check_lse(lse[b, h], rl)
 
 
+def test_gather_attend_long_rows(cuda_lib):
+    """Index lists over rows longer than 2^18 tokens (the bitmap is built in
+    place in global memory, not in shared memory), GQA-union path."""
+    sd = cuda_lib
+    lens = [300_017, 5000]
+    case = workloads.make_case(2, 8, 2, lens, seed=13)
+    dc = _dev(case)
+    kv, _ = _kv(sd, dc)
+    rng = np.random.default_rng(2)
+    k_max = 4000
+    idx = np.full((2, 8, k_max), -1, dtype=np.int32)
+    cnt = np.zeros((2, 8), dtype=np.int32)
+    for b, N in enumerate(lens):
+        for h in range(8):
+            c = int(rng.integers(1, k_max + 1))
+            idx[b, h, :c] = np.sort(rng.choice(N, c, replace=False))
+            cnt[b, h] = c
+    sd.clear_device_error()
+    out, lse = sd.sparse_gather_attend(dc.q, kv, torch.from_numpy(idx).cuda(), torch.from_numpy(cnt).cuda(),
+                                       scale=SCALE, out_dtype=torch.float32)
+    assert sd.read_device_error() == 0
+    out, lse = out.cpu().numpy(), lse.cpu().numpy()
+    inp = oracle.from_case(case)
+    for b in range(2):
+        for h in (0, 3, 6):
+            ro, rl = oracle.attend_given(inp, b, h, idx[b, h, :cnt[b, h]], SCALE)
+            assert rel_err(out[b, h], ro) <= 1e-4
+            check_lse(lse[b, h], rl)
+
+
 def test_gather_attend_device_errors(cuda_lib):
     sd = cuda_lib
     case = _dev(workloads.make_case(1, 4, 1, 100, seed=1))
