@@ -22,7 +22,11 @@
  *    workspace once (sd_clear_device_error) before first use.
  *  - All work is enqueued asynchronously on `stream` (a cudaStream_t; NULL is
  *    the legacy default stream).  The host never synchronizes except in
- *    sd_read_device_error.  No global mutable state: calls are re-entrant.
+ *    sd_read_device_error.  Calls are re-entrant and thread-safe: the only
+ *    state kept between calls is a mutex-guarded per-process record of which
+ *    (device, kernel) pairs already had their shared-memory limit raised
+ *    (an idempotent cudaFuncSetAttribute); all per-call state lives in the
+ *    caller's workspace, so concurrent calls need separate workspaces.
  *  - Host-checked argument errors return SD_ERR_INVALID_ARG and launch nothing.
  *  - Supported specialisations (Table 1 geometry; BASELINE.json):
  *    head_dim == 128, page_size == 16, G = Hq/Hkv in {1,2,4,8},
@@ -222,10 +226,13 @@ sd_status sd_stochastic_select(const sd_geometry* geom, const float* scores, int
  * For every (b, h) with I = idx[b][h][0..counts[b][h]) and weights w (NULL = 1):
  *   s_i = scale <q_bh, K_i>,  a_i = w_i e^{s_i} / sum_j w_j e^{s_j},
  *   out[b][h] = sum_i a_i V_i  (out_dtype),  lse[b][h] = log sum_j w_j e^{s_j}
- * (lse nullable).  Rows are fetched per query head (no GQA dedup: the paper's
- * per-head semantics).  idx entries must be strictly increasing and
+ * (lse nullable).  The result is per query head (the paper's per-head index
+ * sets).  With unit weights (weights == NULL) and bf16 KV the lists
+ * become selection bitmaps and a K/V row chosen by several q-heads of one GQA
+ * group is fetched once (the fused path's union gather-attend); weighted or
+ * fp32 calls gather per head.  idx entries must be strictly increasing and
  * < N_b; violations set the device error word and the offending index is
- * skipped.  weights: fp32 [B][Hq][k_max]. */
+ * skipped (either way).  weights: fp32 [B][Hq][k_max]. */
 sd_status sd_sparse_gather_attend(const sd_geometry* geom, const sd_paged_kv* kv,
                                   const void* q, const int32_t* idx,
                                   const int32_t* counts, int32_t k_max,
@@ -293,10 +300,13 @@ sd_status sd_lse_merge(int32_t parts, int32_t rows, int32_t D, const float* part
 /* ---- Sequence sharding, called around two all-gathers ------
  * Rank r holds a contiguous token shard of every sequence: local token j of
  * sequence b is global token token_offset[b] + j, with shards ordered by rank.
- * (1) sd_seqshard_local_topk: local scores -> the local top-k_b (k_b from the
- *     GLOBAL length global_seq_lens[b]) in the order (score desc, index asc):
- *     cand_scores fp32 [B][Hq][k_max] (unused tail = -inf), cand_idx int32
- *     [B][Hq][k_max] LOCAL indices.
+ * (1) sd_seqshard_local_topk: the local top-min(k_b, N_local) (k_b from the
+ *     GLOBAL length global_seq_lens[b]; order (score desc, index asc), ties to the
+ *     lower index) listed in increasing LOCAL index: cand_idx int32
+ *     [B][Hq][k_max] (unused tail = -1), cand_scores fp32 [B][Hq][k_max] their
+ *     indexer scores (unused tail = -inf).  With a bf16 8-channel sketch and
+ *     G = 4 the fused selection runs (scores never in HBM); otherwise the scores
+ *     are materialised in the workspace and radix-selected.
  * (2) all-gather cand_scores over ranks -> all_cand [P][B][Hq][k_max].
  * (3) sd_seqshard_cut_attend: the global k_b-th element of the P sorted lists
  *     (ties: lower rank first, then lower local position - equal to lower

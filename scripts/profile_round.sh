@@ -7,10 +7,10 @@
 set -u
 OUT=gpurun_out/prof
 mkdir -p $OUT
-CMD="python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-dense"
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-dense --no-graph"
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $OUT/launches.csv $CMD > $OUT/launches.log 2>&1
-for k in sbs_sample_kernel sbs_scan_kernel sbs_select_kernel attend_union_ws_kernel merge_parts_kernel; do
+for k in sbs_sample_mma_kernel sbs_scan_kernel sbs_select_kernel attend_union_ws_kernel merge_parts_kernel; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:"$k" -s 3 -c 1 \
       -o $OUT/$k $CMD > $OUT/$k.log 2>&1
 done

@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["sbs_sample_kernel", "sbs_scan_kernel", "sbs_select_kernel", "attend_union_ws_kernel",
+KERNELS = ["sbs_sample_mma_kernel", "sbs_scan_kernel", "sbs_select_kernel", "attend_union_ws_kernel",
            "merge_parts_kernel"]
 WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Executed Ipc Active", "Issue Slots Busy",
         "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy", "Waves Per SM", "L2 Hit Rate"]
@@ -68,12 +68,13 @@ def full_summary(rep, n_hot=8):
 
 def main():
     src_dir, rnd = sys.argv[1], sys.argv[2]
-    prof = os.path.join(ROOT, "profiles")
+    prof = os.environ.get("PROFILES_DIR", os.path.join(ROOT, "profiles"))
+    os.makedirs(prof, exist_ok=True)
     shutil.copy(os.path.join(src_dir, "launches.csv"), os.path.join(prof, f"{rnd}_launches_cfg3.csv"))
     agg, tot = ncu_summary.summarize(os.path.join(src_dir, "launches.csv"))
     lines = [f"# {rnd}: ncu profile of the fused step at cfg3 (B=16, N=131072, S=50, bf16)", "",
              "Launch list: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-             "--clock-control none python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-dense` "
+             "--clock-control none python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-dense --no-graph` "
              f"(raw: `{rnd}_launches_cfg3.csv`). Durations are serialised and cold-ish (ncu replays); "
              "the kernel SHARE is what bench.py's live `phases_us` must agree with.", "",
              "| kernel | launches | mean us | share | DRAM MB/launch | GB/s |", "|---|---|---|---|---|---|"]
