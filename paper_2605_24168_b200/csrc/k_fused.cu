@@ -1277,6 +1277,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     if constexpr (kWarpLocal) __syncwarp();
     else __syncthreads();
     const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+    const uint32_t st_w = smem_u32(st) + (uint32_t)warp * 32u * 16u;  // this warp's first block of the stage
     const int cb = s * stage_tok;                   // chunk-relative first token of the stage
     const int lim = min(stage_tok, ntok - cb);      // valid tokens of this stage
     const int tbase = t0 + cb;                      // first token of the stage
@@ -1301,7 +1302,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 #pragma unroll
           for (int h = 0; h < kB; ++h) {
             uint32_t a[4];
-            sk_mma_a_smem(a, smem_u32(st + (size_t)(i0 + h * kScanNT + warp * 32) * 16));
+            sk_mma_a_smem(a, st_w + (uint32_t)(i0 + h * kScanNT) * 16u);
             d[h][0] = d[h][1] = d[h][2] = d[h][3] = 0.f;
             sk_mma(d[h], a, qm.b[0]);  // the accumulation order of sk_mma_score
             if constexpr (NP > 1) {
