@@ -671,9 +671,9 @@ def _shard_kv(sd, case, lo, hi):
     return sd.KVCache(case.k_pages, case.v_pages, pt, lens, max(1, int(lens.max()))), lens
 
 
-@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("P,G", [(2, 4), (3, 4), (4, 4), (3, 2)])
 @pytest.mark.parametrize("dist", ["dup", "needle"])
-def test_seqshard_protocol_matches_oracle(cuda_lib, P, dist):
+def test_seqshard_protocol_matches_oracle(cuda_lib, P, G, dist):
     """Sequence sharding on one GPU: local top-k_b per shard ->
     all candidate scores -> global cut + local attend -> LSE merge.  The union
     of the ranks' survivors is bit for bit the exact top-k_b of the GPU's own
@@ -682,7 +682,9 @@ def test_seqshard_protocol_matches_oracle(cuda_lib, P, dist):
     output matches oracle.seqshard_decode and oracle.attend_given on the set."""
     sd = cuda_lib
     N = 8192
-    host = workloads.make_case(2, 16, 4, [N, N - 77], seed=50 + P, dist=dist, n_needles=40)
+    # G = 4: the fused local selection + the GQA-union attend; G = 2: materialised
+    # scores + radix top-k (the general path)
+    host = workloads.make_case(2, 4 * G, 4, [N, N - 77], seed=50 + P, dist=dist, n_needles=40)
     case = _dev(host)
     kv, sk = _kv(sd, case)
     S = 20.0
