@@ -12,7 +12,7 @@ import torch
 
 import oracle
 import workloads
-from parity import (OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_region_selection, check_rows_full_size,
+from parity import (SEL_REL_GAP, OUT_TOL_BF16, OUT_TOL_F32, check_lse, check_region_selection, check_rows_full_size,
                     check_selection, host_subcase, rel_err)
 
 pytestmark = pytest.mark.gpu
@@ -50,6 +50,9 @@ def test_index_score_matches_oracle(cuda_lib, dtype, mode):
             else:
                 mag, n = np.abs(inp.sketch(b, g)) @ np.abs(inp.q[b, h][inp.channel_ids[b, g]]), 8
             assert np.all(np.abs(sc[b, h, :N] - ref) <= n * u * mag + 1e-30), (b, h)
+            # and inside the selection rule's band (1e-5 M_row), so that the rule
+            # tests the selection, not indexer rounding
+            assert np.abs(sc[b, h, :N] - ref).max() <= SEL_REL_GAP * max(np.abs(ref).max(), 1e-30), (b, h)
 
 
 def test_index_score_fp8_sketch_matches_oracle(cuda_lib):
@@ -69,6 +72,7 @@ def test_index_score_fp8_sketch_matches_oracle(cuda_lib):
             g = h // 4
             mag = np.abs(inp.sketch(b, g)) @ np.abs(inp.q[b, h][inp.channel_ids[b, g]])
             assert np.all(np.abs(sc[b, h, :N] - ref) <= 8 * u * mag + 1e-30), (b, h)
+            assert np.abs(sc[b, h, :N] - ref).max() <= SEL_REL_GAP * max(np.abs(ref).max(), 1e-30), (b, h)
 
 
 @pytest.mark.parametrize("dist", ["iid", "needle", "dup"])
