@@ -960,16 +960,30 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
       const SkMmaQ qm = sk_mma_q([qc, jh](int jj, int c) { return jj == jh ? qc[c] : 0.f; }, q_dtype == SD_F32 ? 3 : 1);
       const int u = lane & 3, tofs = (lane >> 2) + ((u >> 1) << 4);
       const bool mine = (u & 1) == (jh >> 1);
-      for (int t0 = warp * 32; t0 < N; t0 += NT) {
-        uint32_t a[4];
-        sk_mma_a_global(a, reinterpret_cast<const uint16_t*>(sk), t0, N,
-                        [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, 8); });
-        float d[4];
-        sk_mma_score(a, qm, d);
-        const int tA = t0 + tofs, tB = tA + 8;
-        const float vA = (jh & 1) ? d[1] : d[0], vB = (jh & 1) ? d[3] : d[2];
-        if (mine && tA < N) sr[tA] = (tA < rb.lo || tA >= rb.hi) ? INFINITY : vA;
-        if (mine && tB < N) sr[tB] = (tB < rb.lo || tB >= rb.hi) ? INFINITY : vB;
+      // 4 blocks per warp in flight (their page ids, then their rows, requested
+      // before any is scored: the loop is latency-bound otherwise)
+      constexpr int kSU = 4;
+      for (int tb = warp * 32; tb < N; tb += kSU * NT) {
+        uint32_t a[kSU][4];
+#pragma unroll
+        for (int x = 0; x < kSU; ++x) {
+          const int t0 = tb + x * NT;
+          if (t0 < N)
+            sk_mma_a_global(a[x], reinterpret_cast<const uint16_t*>(sk), t0, N, [pt, g, Hkv](int t) {
+              return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, 8);
+            });
+        }
+#pragma unroll
+        for (int x = 0; x < kSU; ++x) {
+          const int t0 = tb + x * NT;
+          if (t0 >= N) break;
+          float d[4];
+          sk_mma_score(a[x], qm, d);
+          const int tA = t0 + tofs, tB = tA + 8;
+          const float vA = (jh & 1) ? d[1] : d[0], vB = (jh & 1) ? d[3] : d[2];
+          if (mine && tA < N) sr[tA] = (tA < rb.lo || tA >= rb.hi) ? INFINITY : vA;
+          if (mine && tB < N) sr[tB] = (tB < rb.lo || tB >= rb.hi) ? INFINITY : vB;
+        }
       }
     } else {
       for (int t = tid; t < N; t += NT) {
