@@ -956,7 +956,22 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
     if (tid == 0 && err) atomicAdd(err + 1, 1);  // statistics word: fallback rows
     for (int w = tid; w < nw; w += NT) frh[w] = 0u;
     float* sr = scratch + (size_t)rowh * ld;
-    if (SkMma<G, Sk>::value && C == 8) {  // the scan's tensor-core scores, same MMA placement
+    if (SkMmaF8<G, Sk>::value && C == 8) {  // the fp8 scan's tensor-core scores, same MMA placement
+      const SkMmaF8Q qm8 = sk_mma_q_f8([&](int jj, int c) { return load_q_elem(q, q_dtype, (size_t)(b * Hq + g * G + jj) * kD + __ldg(channel_ids + (size_t)bg * C + c)); });
+      const int u = lane & 3, tofs = (lane >> 2) + ((u >> 1) << 4);
+      const bool mine = (u & 1) == (jh >> 1);
+      for (int t0 = warp * 32; t0 < N; t0 += NT) {
+        uint32_t a[4];
+        sk_f8_a_global(a, reinterpret_cast<const uint8_t*>(sk), t0, N,
+                       [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, 8); });
+        float d[4];
+        sk_mma_score_f8(a, qm8, d);
+        const int tA = t0 + tofs, tB = tA + 8;
+        const float vA = (jh & 1) ? d[1] : d[0], vB = (jh & 1) ? d[3] : d[2];
+        if (mine && tA < N) sr[tA] = (tA < rb.lo || tA >= rb.hi) ? INFINITY : vA;
+        if (mine && tB < N) sr[tB] = (tB < rb.lo || tB >= rb.hi) ? INFINITY : vB;
+      }
+    } else if (SkMma<G, Sk>::value && C == 8) {  // the scan's tensor-core scores, same MMA placement
       const SkMmaQ qm = sk_mma_q([qc, jh](int jj, int c) { return jj == jh ? qc[c] : 0.f; }, q_dtype == SD_F32 ? 3 : 1);
       const int u = lane & 3, tofs = (lane >> 2) + ((u >> 1) << 4);
       const bool mine = (u & 1) == (jh >> 1);
@@ -1058,7 +1073,8 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   constexpr int NW = kScanNT / 32;
   static_assert(NW == kScanWarps, "one band region per scan warp");
   constexpr int CW = band_region_cap(G);
-  constexpr bool kMma = C8 && SkMma<G, Sk>::value;  // tensor-core scores (sd_score.cuh)
+  constexpr bool kF8 = C8 && SkMmaF8<G, Sk>::value;              // fp8 sketch on the tensor cores
+  constexpr bool kMma = C8 && (SkMma<G, Sk>::value || kF8);      // tensor-core scores (sd_score.cuh)
   constexpr bool kWarpLocal = C8 && Sk::kBytes == 2;  // stage rows copied by the warp that scores them
   constexpr int kWords = kRangeTok / 32;              // bitmap words of the chunk, per head
   // per-warp candidate buffer: (token, head pair) entries on the tensor-core
@@ -1185,7 +1201,11 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 
   float qr[G][8];
   SkMmaQ qm;
-  if constexpr (kMma) {
+  SkMmaF8Q qm8;
+  if constexpr (kF8) {
+    qm8 = sk_mma_q_f8(qf);
+    qm.np = 8;  // phase-1 selector: the fp8 path
+  } else if constexpr (kMma) {
     qm = sk_mma_q(qf, q_dtype == SD_F32 ? 3 : 1);
   } else if (C8) {
 #pragma unroll
@@ -1316,12 +1336,17 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
 #pragma unroll
           for (int h = 0; h < kB; ++h) {
             uint32_t a[4];
-            sk_mma_a_smem(a, st_w + (uint32_t)(i0 + h * kScanNT) * 16u);
-            d[h][0] = d[h][1] = d[h][2] = d[h][3] = 0.f;
-            sk_mma(d[h], a, qm.b[0]);  // the accumulation order of sk_mma_score
-            if constexpr (NP > 1) {
-              sk_mma(d[h], a, qm.b[1]);
-              sk_mma(d[h], a, qm.b[2]);
+            if constexpr (NP == 8) {  // fp8 rows of 8 B: the scores of sk_mma_score_f8
+              sk_f8_a_smem(a, smem_u32(st) + (uint32_t)(i0 + h * kScanNT + warp * 32) * 8u);
+              sk_mma_score_f8(a, qm8, d[h]);
+            } else {
+              sk_mma_a_smem(a, st_w + (uint32_t)(i0 + h * kScanNT) * 16u);
+              d[h][0] = d[h][1] = d[h][2] = d[h][3] = 0.f;
+              sk_mma(d[h], a, qm.b[0]);  // the accumulation order of sk_mma_score
+              if constexpr (NP > 1) {
+                sk_mma(d[h], a, qm.b[1]);
+                sk_mma(d[h], a, qm.b[2]);
+              }
             }
           }
 #pragma unroll
@@ -1352,7 +1377,10 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         }
       };
       const bool full = lim == kScanStageTok8 && !edge_stage;
-      if (qm.np == 1) {
+      if constexpr (kF8) {
+        if (full) phase1(std::integral_constant<int, 8>{}, std::true_type{});
+        else phase1(std::integral_constant<int, 8>{}, std::false_type{});
+      } else if (qm.np == 1) {
         if (full) phase1(std::integral_constant<int, 1>{}, std::true_type{});
         else phase1(std::integral_constant<int, 1>{}, std::false_type{});
       } else {
@@ -1691,7 +1719,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   }
   const int nch = (geo.max_seq_len + kRangeTok - 1) / kRangeTok;
   const int sel_cap = band_capacity(geo.max_seq_len, bud, sample_threads(BG, geo.max_seq_len, geo.sms));
-  const bool pair = SkMma<G, Sk>::value && C == 8;
+  const bool pair = (SkMma<G, Sk>::value || SkMmaF8<G, Sk>::value) && C == 8;  // the tensor-core scan's pair regions
   // the region count table: every band region of the longest row, unless the
   // select's shared memory cannot hold it (those rows take the exact slow path)
   int nreg_cap = nch * kScanWarps;

@@ -90,6 +90,50 @@ __global__ void __launch_bounds__(kScanThreads) sketch_score_mma_kernel(
   }
 }
 
+// G = 4, C = 8, fp8 e4m3 sketch: the fp8 tensor-core score of sd_score.cuh
+// (the fused scan's arithmetic and placement).
+__global__ void __launch_bounds__(kScanThreads) sketch_score_mma_f8_kernel(
+    const void* __restrict__ q, int q_dtype, const uint8_t* __restrict__ sk,
+    const int* __restrict__ channel_ids, const int* __restrict__ page_table,
+    const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv, float* __restrict__ scores, int ld) {
+  constexpr int G = 4, C = 8;
+  __shared__ float qc[G * C];
+  const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
+  const int Hq = Hkv * G;
+  const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // invalid rows: not written (topk reports)
+  if (threadIdx.x < G * C) {
+    const int j = threadIdx.x / C, c = threadIdx.x - j * C;
+    const int ch = __ldg(channel_ids + ((size_t)b * Hkv + g) * C + c);
+    const size_t qe = ((size_t)b * Hq + g * G + j) * kD + ch;
+    qc[threadIdx.x] = q_dtype == SD_F32 ? reinterpret_cast<const float*>(q)[qe]
+                                        : bf_lo(reinterpret_cast<const uint16_t*>(q)[qe]);
+  }
+  __syncthreads();
+  const SkMmaF8Q qm = sk_mma_q_f8([](int j, int c) { return qc[j * C + c]; });
+  const int* pt = page_table + (size_t)b * max_pages;
+  const int tbeg = blockIdx.x * kScanTok;
+  const int tend = min(N, tbeg + kScanTok);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, u = lane & 3;
+  const int tofs = (lane >> 2) + ((u >> 1) << 4), h0 = 2 * (u & 1);
+  float* srow = scores + ((size_t)b * Hq + g * G) * ld;
+  for (int t0 = tbeg + warp * 32; t0 < tend; t0 += kScanThreads) {
+    uint32_t a[4];
+    sk_f8_a_global(a, sk, t0, tend,
+                   [pt, g, Hkv](int t) { return sketch_row_elem(__ldg(pt + (t >> 4)), t & 15, g, Hkv, C); });
+    float d[4];
+    sk_mma_score_f8(a, qm, d);
+    const int tA = t0 + tofs, tB = tA + 8;
+    if (tA < tend) {
+      srow[(size_t)h0 * ld + tA] = d[0];
+      srow[(size_t)(h0 + 1) * ld + tA] = d[1];
+    }
+    if (tB < tend) {
+      srow[(size_t)h0 * ld + tB] = d[2];
+      srow[(size_t)(h0 + 1) * ld + tB] = d[3];
+    }
+  }
+}
+
 // Exact scores from the K pages: one half-warp per token row, kExUnroll rows
 // per half-warp in flight (their page ids, then their K rows, are requested
 // before any is used), kExTok tokens per CTA so that short rows still spread
@@ -146,7 +190,11 @@ cudaError_t index_dispatch(const Geo& g, const sd_paged_kv& kv, const sd_sketch*
   dim3 grid((g.max_seq_len + kScanTok - 1) / kScanTok, g.B * g.Hkv);
   if (sk) {
     const size_t smem = sizeof(float) * G * sk->channels;
-    if (sk->dtype == SD_E4M3)
+    if (sk->dtype == SD_E4M3 && G == 4 && sk->channels == 8)
+      sketch_score_mma_f8_kernel<<<grid, kScanThreads, 0, st>>>(
+          q, g.kv_dtype, reinterpret_cast<const uint8_t*>(sk->pages), sk->channel_ids, kv.page_table, kv.seq_lens,
+          g.max_seq_len, g.max_pages, g.Hkv, scores, ld);
+    else if (sk->dtype == SD_E4M3)
       sketch_score_kernel<G, SkE4m3><<<grid, kScanThreads, smem, st>>>(
           q, g.kv_dtype, sk->pages, sk->channel_ids, sk->channels, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hkv,
           scores, ld);

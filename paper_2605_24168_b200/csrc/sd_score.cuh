@@ -133,6 +133,90 @@ __device__ __forceinline__ void sk_mma_a_global(uint32_t (&a)[4], const uint16_t
   }
 }
 
+// ---- G = 4, C = 8, fp8 e4m3 sketch on the tensor cores (NEXT-4).  The e4m3
+// channel values convert exactly to f16 (cvt.rn.f16x2.e4m3x2); the f16 MMA
+// (fp32 accumulate) multiplies them with q * 2^s split into two f16 parts
+// hi + lo (accumulated in that order), s = 14 - ilogb(max |q| over the group's
+// 4 heads x 8 channels), so no part overflows and every q value above 2^-24 of
+// that maximum is represented; the result is scaled back by 2^-s (exact).  Same
+// fragment placement as SkMma (32-token blocks from multiples of 32), the same
+// in every kernel that scores an fp8 sketch with it (fused scan, select slow
+// path, unfused indexer), so a (token, head) score is the same bits everywhere.
+template <int G, class Sk>
+struct SkMmaF8 {
+  static constexpr bool value = false;
+};
+template <>
+struct SkMmaF8<4, SkE4m3> {
+  static constexpr bool value = true;
+};
+struct SkMmaF8Q {
+  uint32_t b[2][2];
+  float unscale;
+};
+template <class QF>
+__device__ __forceinline__ SkMmaF8Q sk_mma_q_f8(QF qf) {
+  const int lane = threadIdx.x & 31, n = lane >> 2, u = lane & 3;
+  const int head = n & 3, grp = n >> 2;
+  float v0 = qf(head, 2 * u), v1 = qf(head, 2 * u + 1);
+  float m = fmaxf(fabsf(v0), fabsf(v1));  // lanes 0-15 hold all 4 x 8 values (16-31 repeat them)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int sc = m > 0.f ? min(max(14 - ilogbf(m), -120), 120) : 0;
+  v0 = ldexpf(v0, sc);
+  v1 = ldexpf(v1, sc);
+  SkMmaF8Q r;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+    const uint32_t w = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+    r.b[p][0] = grp == 0 ? w : 0u;
+    r.b[p][1] = grp == 0 ? 0u : w;
+    v0 -= __half2float(h0);
+    v1 -= __half2float(h1);
+  }
+  r.unscale = ldexpf(1.f, -sc);
+  return r;
+}
+__device__ __forceinline__ uint32_t f8x2_to_f16x2(uint16_t pair) {
+  const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)pair, __NV_E4M3);
+  return (uint32_t)h.x | ((uint32_t)h.y << 16);
+}
+__device__ __forceinline__ void sk_mma_f16(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void sk_mma_score_f8(const uint32_t (&a)[4], const SkMmaF8Q& q, float (&d)[4]) {
+  d[0] = d[1] = d[2] = d[3] = 0.f;
+  sk_mma_f16(d, a, q.b[0]);
+  sk_mma_f16(d, a, q.b[1]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] *= q.unscale;
+}
+// A fragment of tokens t0 .. t0+31 from 8-B e4m3 rows in shared memory (row i at base + 8 i).
+__device__ __forceinline__ void sk_f8_a_smem(uint32_t (&a)[4], uint32_t base) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, u = lane & 3;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(base + (uint32_t)(8 * m + r) * 8u + 2u * u));
+    a[m] = f8x2_to_f16x2(v);
+  }
+}
+// A fragment from global memory: row(t) -> byte offset of token t's 8-B row (t < n).
+template <class RowByte>
+__device__ __forceinline__ void sk_f8_a_global(uint32_t (&a)[4], const uint8_t* sk, int t0, int n, RowByte row) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, u = lane & 3;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int t = t0 + 8 * m + r;
+    a[m] = t < n ? f8x2_to_f16x2(__ldg(reinterpret_cast<const uint16_t*>(sk + row(t)) + u)) : 0u;
+  }
+}
+
 // Sketch row address (elements) of token (page, slot) for KV head g.
 __device__ __forceinline__ size_t sketch_row_elem(int page, int slot, int g, int Hkv, int C) {
   return ((size_t)(page * Hkv + g) * kPS + slot) * C;
