@@ -1075,7 +1075,8 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   constexpr int CW = band_region_cap(G);
   constexpr bool kF8 = C8 && SkMmaF8<G, Sk>::value;              // fp8 sketch on the tensor cores
   constexpr bool kMma = C8 && (SkMma<G, Sk>::value || kF8);      // tensor-core scores (sd_score.cuh)
-  constexpr bool kWarpLocal = C8 && Sk::kBytes == 2;  // stage rows copied by the warp that scores them
+  // stage rows copied by the warp that scores them (bf16 rows; fp8 rows on the tensor-core path)
+  constexpr bool kWarpLocal = C8 && (Sk::kBytes == 2 || SkMmaF8<G, Sk>::value);
   constexpr int kWords = kRangeTok / 32;              // bitmap words of the chunk, per head
   // per-warp candidate buffer: (token, head pair) entries on the tensor-core
   // path, (token) entries otherwise; flushed (phase 2) before a block could overflow it
@@ -1148,7 +1149,22 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   auto issue = [&](int s) {
     if (s < nst) {
       unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
-      if (C8) {
+      if (C8 && SkMmaF8<G, Sk>::value) {
+        // fp8 rows, tensor-core path: warp w copies its own 4 blocks of 32 tokens
+        // (stage tokens 256 j + 32 w + [0, 32)), 2 tokens per 16-B copy, so a warp
+        // only waits for its own lanes' copies
+        const bool whole = (s + 1) * kScanStageTok8 <= ntok;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = lane + 32 * e, ti = 256 * (c >> 4) + 32 * warp + 2 * (c & 15);
+          if (whole || s * kScanStageTok8 + ti < ntok) {
+            const int pg = s_pages[(s * kScanStageTok8 + ti) >> 4];
+            const char* src = skb + ((size_t)((uint32_t)pg * Hkv + g) * kPS + (ti & 15)) * 8;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(st + (size_t)ti * 8)), "l"(src)
+                         : "memory");
+          }
+        }
+      } else if (C8) {
         const int* sp = s_pages + (s * kScanStageTok8 >> 4) + ((tid * kTpc) >> 4);
         if ((s + 1) * kScanStageTok8 <= ntok) {  // full stage: plain copies
 #pragma unroll

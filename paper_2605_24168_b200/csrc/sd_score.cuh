@@ -138,10 +138,14 @@ __device__ __forceinline__ void sk_mma_a_global(uint32_t (&a)[4], const uint16_t
 // (fp32 accumulate) multiplies them with q * 2^s split into two f16 parts
 // hi + lo (accumulated in that order), s = 14 - ilogb(max |q| over the group's
 // 4 heads x 8 channels), so no part overflows and every q value above 2^-24 of
-// that maximum is represented; the result is scaled back by 2^-s (exact).  Same
-// fragment placement as SkMma (32-token blocks from multiples of 32), the same
-// in every kernel that scores an fp8 sketch with it (fused scan, select slow
-// path, unfused indexer), so a (token, head) score is the same bits everywhere.
+// that maximum is represented; the result is scaled back by 2^-s (exact).
+// Placement (32 tokens t0 .. t0+31, t0 a multiple of 32): A row r holds token
+// r (k slots of lanes u = 0, 1) and token r + 16 (u = 2, 3); lane (r, u) reads
+// channels 4 (u & 1) .. +3 of its token as ONE 32-bit word (a0 / a2 = its low /
+// high channel pairs; a1 / a3 the same for token + 8), B is permuted to match,
+// and D is laid out exactly as SkMma's (lane (r, u): heads 2 (u & 1), +1 of
+// tokens r + 16 (u >> 1) and + 8).  The same in every kernel that scores an fp8
+// sketch with it (fused scan, select slow path, unfused indexer).
 template <int G, class Sk>
 struct SkMmaF8 {
   static constexpr bool value = false;
@@ -154,26 +158,33 @@ struct SkMmaF8Q {
   uint32_t b[2][2];
   float unscale;
 };
+__device__ __forceinline__ uint32_t f16x2_bits(float lo, float hi) {
+  return (uint32_t)__half_as_ushort(__float2half_rn(lo)) | ((uint32_t)__half_as_ushort(__float2half_rn(hi)) << 16);
+}
 template <class QF>
 __device__ __forceinline__ SkMmaF8Q sk_mma_q_f8(QF qf) {
   const int lane = threadIdx.x & 31, n = lane >> 2, u = lane & 3;
-  const int head = n & 3, grp = n >> 2;
-  float v0 = qf(head, 2 * u), v1 = qf(head, 2 * u + 1);
-  float m = fmaxf(fabsf(v0), fabsf(v1));  // lanes 0-15 hold all 4 x 8 values (16-31 repeat them)
+  const int head = n & 3, c0 = 4 * (u & 1);
+  const bool live = (u >> 1) == (n >> 2);  // the k slots of token group u >> 1 feed columns of group n >> 2
+  float v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = qf(head, c0 + i);
+  float m = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int sc = m > 0.f ? min(max(14 - ilogbf(m), -120), 120) : 0;
-  v0 = ldexpf(v0, sc);
-  v1 = ldexpf(v1, sc);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = ldexpf(v[i], sc);
   SkMmaF8Q r;
 #pragma unroll
   for (int p = 0; p < 2; ++p) {
-    const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-    const uint32_t w = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-    r.b[p][0] = grp == 0 ? w : 0u;
-    r.b[p][1] = grp == 0 ? 0u : w;
-    v0 -= __half2float(h0);
-    v1 -= __half2float(h1);
+    float h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __half2float(__float2half_rn(v[i]));
+    r.b[p][0] = live ? f16x2_bits(v[0], v[1]) : 0u;  // k = 2u, 2u + 1: channels c0, c0 + 1
+    r.b[p][1] = live ? f16x2_bits(v[2], v[3]) : 0u;  // k = 2u + 8, 2u + 9: channels c0 + 2, c0 + 3
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] -= h[i];
   }
   r.unscale = ldexpf(1.f, -sc);
   return r;
@@ -181,6 +192,12 @@ __device__ __forceinline__ SkMmaF8Q sk_mma_q_f8(QF qf) {
 __device__ __forceinline__ uint32_t f8x2_to_f16x2(uint16_t pair) {
   const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)pair, __NV_E4M3);
   return (uint32_t)h.x | ((uint32_t)h.y << 16);
+}
+__device__ __forceinline__ void sk_f8_frag(uint32_t (&a)[4], uint32_t w0, uint32_t w1) {
+  a[0] = f8x2_to_f16x2((uint16_t)(w0 & 0xFFFFu));
+  a[2] = f8x2_to_f16x2((uint16_t)(w0 >> 16));
+  a[1] = f8x2_to_f16x2((uint16_t)(w1 & 0xFFFFu));
+  a[3] = f8x2_to_f16x2((uint16_t)(w1 >> 16));
 }
 __device__ __forceinline__ void sk_mma_f16(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
   asm volatile(
@@ -199,22 +216,20 @@ __device__ __forceinline__ void sk_mma_score_f8(const uint32_t (&a)[4], const Sk
 // A fragment of tokens t0 .. t0+31 from 8-B e4m3 rows in shared memory (row i at base + 8 i).
 __device__ __forceinline__ void sk_f8_a_smem(uint32_t (&a)[4], uint32_t base) {
   const int lane = threadIdx.x & 31, r = lane >> 2, u = lane & 3;
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    uint16_t v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(base + (uint32_t)(8 * m + r) * 8u + 2u * u));
-    a[m] = f8x2_to_f16x2(v);
-  }
+  const uint32_t p = base + (uint32_t)(r + ((u >> 1) << 4)) * 8u + 4u * (u & 1);
+  uint32_t w0, w1;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(p));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w1) : "r"(p + 64u));
+  sk_f8_frag(a, w0, w1);
 }
 // A fragment from global memory: row(t) -> byte offset of token t's 8-B row (t < n).
 template <class RowByte>
 __device__ __forceinline__ void sk_f8_a_global(uint32_t (&a)[4], const uint8_t* sk, int t0, int n, RowByte row) {
   const int lane = threadIdx.x & 31, r = lane >> 2, u = lane & 3;
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const int t = t0 + 8 * m + r;
-    a[m] = t < n ? f8x2_to_f16x2(__ldg(reinterpret_cast<const uint16_t*>(sk + row(t)) + u)) : 0u;
-  }
+  const int ta = t0 + r + ((u >> 1) << 4), tb = ta + 8;
+  const uint32_t w0 = ta < n ? __ldg(reinterpret_cast<const uint32_t*>(sk + row(ta)) + (u & 1)) : 0u;
+  const uint32_t w1 = tb < n ? __ldg(reinterpret_cast<const uint32_t*>(sk + row(tb)) + (u & 1)) : 0u;
+  sk_f8_frag(a, w0, w1);
 }
 
 // Sketch row address (elements) of token (page, slot) for KV head g.
