@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(kAttThreads) attend_list_kernel(
   const int row = blockIdx.y, split = blockIdx.x;
   const int b = row / Hq, h = row - b * Hq, g = h / (Hq / Hkv);
   const int N = seq_len_dev(seq_lens, b, max_len);  // -1 (out of range): every count is rejected
-  int cnt = __ldg(counts + row);
+  pdl_wait();  // idx / counts / weights may come from the preceding kernel (coherent loads below)
+  int cnt = __ldcg(counts + row);
   if ((cnt < 1 && !allow_empty) || cnt > k_max || cnt > N) {
     if (split == 0 && threadIdx.x == 0) set_error(err, cnt < 1 ? SD_DEVERR_EMPTY : SD_DEVERR_SEQLEN);
     cnt = max(0, min(cnt, min(k_max, max(N, 0))));
@@ -100,16 +101,16 @@ __global__ void __launch_bounds__(kAttThreads) attend_list_kernel(
       ok[u] = false;
       xb[u] = 0.f;
       if (e < c1) {
-        t = __ldg(ip + e);
+        t = __ldcg(ip + e);
         ok[u] = (t >= 0) && (t < N);
-        if (ok[u] && e > 0 && __ldg(ip + e - 1) >= t) {
+        if (ok[u] && e > 0 && __ldcg(ip + e - 1) >= t) {
           ok[u] = false;
           if (l16 == 0) set_error(err, SD_DEVERR_INDEX_ORDER);
         } else if (!ok[u] && l16 == 0) {
           set_error(err, SD_DEVERR_INDEX_RANGE);
         }
         if (ok[u] && wp) {
-          const float w = __ldg(wp + e);
+          const float w = __ldcg(wp + e);
           if (!(w > 0.f) || !isfinite(w)) {
             ok[u] = false;
             if (l16 == 0) set_error(err, SD_DEVERR_WEIGHT);
@@ -267,24 +268,30 @@ cudaError_t launch_attend_list(const Geo& g, const sd_paged_kv& kv, const void* 
                                const int* idx, const int* counts, int k_max,
                                const float* weights, float scale, float* part, int splits,
                                int allow_empty, int* err, cudaStream_t st) {
-  dim3 grid(splits, g.B * g.Hq);
   const float sl2 = scale * kLog2e;
+  // programmatic dependent launch: the launch overlaps the preceding kernel's tail
+  // (the kernel waits for it before reading idx / counts / weights)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(splits, g.B * g.Hq);
+  cfg.blockDim = dim3(kAttThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (g.kv_dtype == SD_BF16)
-    attend_list_kernel<KvBF16><<<grid, kAttThreads, 0, st>>>(
-        q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hq, g.Hkv, idx,
-        counts, k_max, weights, sl2, part, splits, allow_empty, err);
-  else
-    attend_list_kernel<KvF32><<<grid, kAttThreads, 0, st>>>(
-        q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens, g.max_seq_len, g.max_pages, g.Hq, g.Hkv, idx,
-        counts, k_max, weights, sl2, part, splits, allow_empty, err);
-  return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, attend_list_kernel<KvBF16>, q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens,
+                              g.max_seq_len, g.max_pages, g.Hq, g.Hkv, idx, counts, k_max, weights, sl2, part, splits,
+                              allow_empty, err);
+  return cudaLaunchKernelEx(&cfg, attend_list_kernel<KvF32>, q, kv.k_pages, kv.v_pages, kv.page_table, kv.seq_lens,
+                            g.max_seq_len, g.max_pages, g.Hq, g.Hkv, idx, counts, k_max, weights, sl2, part, splits,
+                            allow_empty, err);
 }
 
 cudaError_t launch_merge_parts(const float* part, int rows, int splits, void* out,
                                int out_dtype, float* lse, cudaStream_t st) {
-  if (splits > 4 * 128) return cudaErrorInvalidValue;  // merge_parts_kernel bound
-  merge_parts_kernel<<<rows, 128, 0, st>>>(part, splits, out, out_dtype, lse);
-  return cudaGetLastError();
+  return launch_merge_parts_pdl(part, rows, splits, out, out_dtype, lse, st);
 }
 
 cudaError_t launch_merge_parts_pdl(const float* part, int rows, int splits, void* out, int out_dtype, float* lse,

@@ -20,12 +20,13 @@ constexpr int kTkThreads = 1024;
 // shard); the selection runs over the local N_b and keeps min(k_b, N_b).
 // out_scores (nullable): the selected scores, same order as idx; slots
 // [count, k_max) of idx/out_scores are padded with -1 / -inf when pad != 0.
-__global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
+template <int NT>
+__global__ void __launch_bounds__(NT) topk_radix_kernel(
     const float* __restrict__ scores, int ld, const int* __restrict__ seq_lens, int max_len,
     const int* __restrict__ k_from, int max_from, int Hq, BudgetDev bud, int* __restrict__ idx,
     int* __restrict__ counts, float* __restrict__ out_scores, int k_max, int pad,
     int* __restrict__ err) {
-  __shared__ SelectSmem<kTkThreads> sm;
+  __shared__ SelectSmem<NT> sm;
   const int row = blockIdx.x, b = row / Hq, tid = threadIdx.x;
   const int N = seq_len_dev(seq_lens, b, max_len);  // -1: out of range (SEQLEN below)
   const bool regions = !k_from && budget_regions(bud);
@@ -47,19 +48,20 @@ __global__ void __launch_bounds__(kTkThreads) topk_radix_kernel(
     return;
   }
   const float* s = scores + (size_t)row * ld;
-  auto key_at = [s, lo, hi](int i) { return (i < lo || i >= hi) ? 0xFFFFFFFFu : score_key(__ldg(s + i)); };
+  pdl_wait();  // the scores come from the preceding kernel (coherent loads)
+  auto key_at = [s, lo, hi](int i) { return (i < lo || i >= hi) ? 0xFFFFFFFFu : score_key(__ldcg(s + i)); };
   uint32_t emitted = 0;
   if (k > 0) {
     uint32_t tau, need_eq;
-    radix_select_block<kTkThreads>(key_at, N, (uint32_t)k, sm, &tau, &need_eq);
-    emitted = emit_block<kTkThreads, 4>(key_at, N, tau, need_eq, 0u, sm,
+    radix_select_block<NT>(key_at, N, (uint32_t)k, sm, &tau, &need_eq);
+    emitted = emit_block<NT, 4>(key_at, N, tau, need_eq, 0u, sm,
                                         [out, osc](uint32_t pos, int i, uint32_t key) {
                                           out[pos] = i;
                                           if (osc) osc[pos] = key_score(key);
                                         });
   }
   if (pad) {
-    for (int j = (int)emitted + tid; j < k_max; j += kTkThreads) {
+    for (int j = (int)emitted + tid; j < k_max; j += NT) {
       out[j] = -1;
       if (osc) osc[j] = -INFINITY;
     }
@@ -123,15 +125,24 @@ __global__ void __launch_bounds__(kTkThreads) seqshard_cut_kernel(
 
 cudaError_t launch_topk(const Geo& g, const float* scores, int ld, const int* seq_lens,
                         Budget bud, int* idx, int* counts, int k_max, int* err, cudaStream_t st) {
-  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, g.max_seq_len, nullptr, 0, g.Hq, bud.dev(),
-                                                       idx, counts, nullptr, k_max, 0, err);
-  return cudaGetLastError();
+  // programmatic dependent launch (the kernel waits before reading the scores)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.B * g.Hq);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(kTkThreads);  // (256-thread CTAs for short rows measured slower: cfg1 38 -> 50 us)
+  return cudaLaunchKernelEx(&cfg, topk_radix_kernel<kTkThreads>, scores, ld, seq_lens, g.max_seq_len,
+                            (const int*)nullptr, 0, g.Hq, bud.dev(), idx, counts, (float*)nullptr, k_max, 0, err);
 }
 
 cudaError_t launch_topk_shard(const Geo& g, const float* scores, int ld, const int* seq_lens,
                               const int* global_lens, int max_global, Budget bud, int* idx, int* counts,
                               float* cand_scores, int k_max, int* err, cudaStream_t st) {
-  topk_radix_kernel<<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, g.max_seq_len, global_lens, max_global,
+  topk_radix_kernel<kTkThreads><<<g.B * g.Hq, kTkThreads, 0, st>>>(scores, ld, seq_lens, g.max_seq_len, global_lens, max_global,
                                                        g.Hq, bud.dev(),
                                                        idx, counts, cand_scores, k_max, 1,
                                                        err);
