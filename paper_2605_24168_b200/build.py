@@ -38,6 +38,7 @@ def _flags(debug: bool):
     f = ["-std=c++17", GENCODE, "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
          "--expt-relaxed-constexpr", "--extended-lambda", "-Xptxas", "-v"]
     f += ["-O0", "-G"] if debug else ["-O3"]
+    f += os.environ.get("SD_NVCC_EXTRA", "").split()  # build-time variants (A/B experiments)
     return f
 
 
