@@ -74,6 +74,9 @@ constexpr int kScanCandCap = kScanStageTok8 / 8;    // candidates per warp per s
 constexpr int kSelNT = 256;           // 4 CTAs per SM: B*Hq = 512 rows in one wave
 constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
 constexpr int kTieCap = 2048;
+#ifndef SD_SEL_UQ
+#define SD_SEL_UQ 6  // select, pair regions: entries per lane requested with the region count
+#endif
 
 __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t e) {
   return q_dtype == SD_F32 ? reinterpret_cast<const float*>(q)[e]
@@ -732,113 +735,167 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
   const uint32_t lo = thr[row * 4 + 0], hi = thr[row * 4 + 1];
   const int nw = (N + 31) >> 5;
   __syncthreads();
-  // ---- sure count: the scan's bits of the half's row
-  {
-    int sure = 0;
-    for (int w = ht; w < nw; w += kSelNT) sure += __popc(fr[w]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
-    if (lane == 0 && sure) atomicAdd(&s_sure[h], sure);
-  }
-  // ---- band entries: warp per region over the whole CTA
-  int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
-  if (nreg > a.nreg_cap) {  // count table too small (beyond the shared memory): exact slow path
-    nreg = 0;
-    if (tid < HPC) s_fb[tid] = 1;
-  }
   const uint32_t lt = (1u << lane) - 1u;
-  // band regions: union format (one per scan warp, G scores per entry) or, on
-  // the tensor-core scan (Pair), one per (scan warp, head pair) with the
-  // pair's 2 scores per entry
-  constexpr int nsub = Pair ? 2 : 1, nh = Pair ? 2 : G;
+  constexpr int nh = Pair ? 2 : G;
   const int sub = Pair ? (j0 >> 1) : 0, e0 = Pair ? (j0 & 1) : j0;  // score index of head slot 0 (Two: 0)
-  const size_t reg0 = (size_t)bg * nch * NW;
-  auto greg = [&](int r) { return (reg0 + r) * nsub + sub; };
-  // region counts -> shared memory in one coalesced pass (overflow: slow path)
-  int* s_cnt = reinterpret_cast<int*>(qc0 + HPC * C);  // [nreg]
-  for (int r = tid; r < nreg; r += NT) {
-    int c = ent_cnt[greg(r)];
-    if (c > CW) {
-      for (int hh = 0; hh < HPC; ++hh) s_fb[hh] = 1;
-      c = 0;
-    }
-    s_cnt[r] = c;
-  }
-  __syncthreads();
-  // warp per region with RQ regions in flight: entries lane + 32 u (u < UQ) of
-  // each are loaded before any is used; longer regions finish in a tail loop.
-  // Each entry is kept for every head slot whose mask bit it carries.
-  constexpr int RQ = 4, UQ = 2;
-  auto keep_group = [&](const uint32_t (&tk)[RQ][UQ], const float (&sc)[RQ][UQ][HPC], int nq) {
+  // Keep KQ loaded entries (token | mask << 24, HPC scores each) for every head
+  // slot whose mask bit they carry: per slot one warp ballot per entry, one
+  // shared-memory atomic per warp for the positions.
+  auto keep_entries = [&](auto kq_tag, const uint32_t* tk, const float* sc) {
+    constexpr int KQ = decltype(kq_tag)::value;
 #pragma unroll
     for (int hh = 0; hh < HPC; ++hh) {
       const uint32_t jbit = 1u << (24 + e0 + hh);
       uint32_t* keys = keys0 + hh * sel_cap;
       uint32_t* toks = toks0 + hh * sel_cap;
-      uint32_t bal[RQ][UQ];
+      uint32_t bal[KQ];
       int tot = 0;
 #pragma unroll
-      for (int qq = 0; qq < RQ; ++qq)
-#pragma unroll
-        for (int u = 0; u < UQ; ++u) {
-          bal[qq][u] = qq < nq ? __ballot_sync(0xffffffffu, (tk[qq][u] & jbit) != 0u) : 0u;
-          tot += __popc(bal[qq][u]);
-        }
+      for (int u = 0; u < KQ; ++u) {
+        bal[u] = __ballot_sync(0xffffffffu, (tk[u] & jbit) != 0u);
+        tot += __popc(bal[u]);
+      }
       if (tot) {
         int base = 0;
         if (lane == 0) base = atomicAdd(&s_n[hh], tot);
         base = __shfl_sync(0xffffffffu, base, 0);
 #pragma unroll
-        for (int qq = 0; qq < RQ; ++qq)
-#pragma unroll
-          for (int u = 0; u < UQ; ++u) {
-            const int p = base + __popc(bal[qq][u] & lt);
-            if ((bal[qq][u] >> lane) & 1u && p < sel_cap) {
-              keys[p] = score_key(sc[qq][u][hh]);
-              toks[p] = tk[qq][u] & 0x00FFFFFFu;
-            }
-            base += __popc(bal[qq][u]);
+        for (int u = 0; u < KQ; ++u) {
+          const int p = base + __popc(bal[u] & lt);
+          if ((bal[u] >> lane) & 1u && p < sel_cap) {
+            keys[p] = score_key(sc[u * HPC + hh]);
+            toks[p] = tk[u] & 0x00FFFFFFu;
           }
+          base += __popc(bal[u]);
+        }
       }
     }
   };
-  for (int rb0 = warp; rb0 < nreg; rb0 += (NT / 32) * RQ) {
-    uint32_t tk[RQ][UQ];
-    float sc[RQ][UQ][HPC];
-    int cnt[RQ];
+  auto sure_count = [&]() {  // the scan's bits of the half's row (all its loads in one round)
+    int sure = 0;
+    const uint2* fr2 = reinterpret_cast<const uint2*>(fr);  // ldw is even: 8-B aligned rows
+    const int nw2 = (nw + 1) >> 1;
+#pragma unroll 8
+    for (int w = ht; w < nw2; w += kSelNT) {
+      uint2 v = fr2[w];
+      if (2 * w + 1 >= nw) v.y = 0u;  // the word past N_b is not the scan's
+      sure += __popc(v.x) + __popc(v.y);
+    }
 #pragma unroll
-    for (int qq = 0; qq < RQ; ++qq) {
-      const int r = rb0 + (NT / 32) * qq;
-      cnt[qq] = r < nreg ? s_cnt[r] : 0;
-      const uint32_t* rtok = ent_tok + greg(r) * CW;
-      const float* rsc = ent_sc + greg(r) * CW * nh + e0;
+    for (int o = 16; o > 0; o >>= 1) sure += __shfl_xor_sync(0xffffffffu, sure, o);
+    if (lane == 0 && sure) atomicAdd(&s_sure[h], sure);
+  };
+  if constexpr (Pair) {
+    // ---- band entries of the tensor-core scan: one region per (8192-token
+    // chunk, head pair), written by the scan CTA's 8 warps (capacity
+    // kScanWarps * CW).  Warp w takes chunks w, w + NT/32, ...; its lanes request
+    // entries lane + 32 u (u < kUQ) together with the region's count, so the
+    // counts, the entries and the sure-count words arrive in one memory round
+    // trip; entries past the count are dropped, longer regions finish in rounds
+    // of kUT * 32.
+    constexpr int kCWC = NW * CW;
+    constexpr int kUQ = SD_SEL_UQ, kUT = 4;
+    const int nchr = (N + kRangeTok - 1) / kRangeTok;
+    for (int c0 = warp; c0 < nchr; c0 += NT / 32) {
+      const size_t cr = ((size_t)bg * nch + c0) * 2 + sub;
+      const uint32_t* rtok = ent_tok + cr * kCWC;
+      const float* rsc = ent_sc + cr * kCWC * 2 + e0;
+      uint32_t tk[kUQ];
+      float sc[kUQ * HPC];
 #pragma unroll
-      for (int u = 0; u < UQ; ++u) {
+      for (int u = 0; u < kUQ; ++u) {
         const int i = lane + 32 * u;
-        tk[qq][u] = i < cnt[qq] ? rtok[i] : 0u;
+        tk[u] = rtok[i];
         if constexpr (HPC == 2) {
-          const float2 v = i < cnt[qq] ? *reinterpret_cast<const float2*>(rsc + (size_t)i * nh) : make_float2(0.f, 0.f);
-          sc[qq][u][0] = v.x;
-          sc[qq][u][HPC - 1] = v.y;
+          const float2 v = *reinterpret_cast<const float2*>(rsc + (size_t)i * 2);
+          sc[2 * u] = v.x;
+          sc[2 * u + 1] = v.y;
         } else {
-          sc[qq][u][0] = i < cnt[qq] ? rsc[(size_t)i * nh] : 0.f;
+          sc[u] = rsc[(size_t)i * 2];
         }
       }
-    }
-    keep_group(tk, sc, RQ);
-    // tail: regions longer than 32 UQ entries
-    for (int qq = 0; qq < RQ; ++qq) {
-      const int r = rb0 + (NT / 32) * qq;
-      for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
-        uint32_t tk1[RQ][UQ] = {};
-        float sc1[RQ][UQ][HPC] = {};
-        const int i = i0 + lane;
-        if (i < cnt[qq]) {
-          tk1[0][0] = ent_tok[greg(r) * CW + i];
+      int cnt = ent_cnt[cr];
+      if (c0 == warp) sure_count();  // (first pass only) its loads overlap the entries'
+      if (cnt > kCWC) {  // region overflow: exact slow path
+        for (int hh = 0; hh < HPC; ++hh) s_fb[hh] = 1;
+        cnt = 0;
+      }
 #pragma unroll
-          for (int hh = 0; hh < HPC; ++hh) sc1[0][0][hh] = ent_sc[(greg(r) * CW + i) * nh + e0 + hh];
+      for (int u = 0; u < kUQ; ++u)
+        if (lane + 32 * u >= cnt) tk[u] = 0u;
+      keep_entries(std::integral_constant<int, kUQ>{}, tk, sc);
+      for (int i0 = 32 * kUQ; i0 < cnt; i0 += 32 * kUT) {
+        uint32_t tk1[kUT];
+        float sc1[kUT * HPC];
+#pragma unroll
+        for (int u = 0; u < kUT; ++u) {
+          const int i = i0 + lane + 32 * u;
+          tk1[u] = i < cnt ? rtok[i] : 0u;
+#pragma unroll
+          for (int hh = 0; hh < HPC; ++hh) sc1[u * HPC + hh] = i < cnt ? rsc[(size_t)i * 2 + hh] : 0.f;
         }
-        keep_group(tk1, sc1, 1);
+        keep_entries(std::integral_constant<int, kUT>{}, tk1, sc1);
+      }
+    }
+    if (warp >= nchr) sure_count();
+  } else {
+    sure_count();
+    // ---- band entries (union format: one region per scan warp, G scores per
+    // entry): warp per region over the whole CTA
+    int nreg = ((N + kRangeTok - 1) / kRangeTok) * NW;
+    if (nreg > a.nreg_cap) {  // count table too small (beyond the shared memory): exact slow path
+      nreg = 0;
+      if (tid < HPC) s_fb[tid] = 1;
+    }
+    const size_t reg0 = (size_t)bg * nch * NW;
+    auto greg = [&](int r) { return reg0 + r; };
+    // region counts -> shared memory in one coalesced pass (overflow: slow path)
+    int* s_cnt = reinterpret_cast<int*>(qc0 + HPC * C);  // [nreg]
+    for (int r = tid; r < nreg; r += NT) {
+      int c = ent_cnt[greg(r)];
+      if (c > CW) {
+        for (int hh = 0; hh < HPC; ++hh) s_fb[hh] = 1;
+        c = 0;
+      }
+      s_cnt[r] = c;
+    }
+    __syncthreads();
+    // warp per region with RQ regions in flight: entries lane + 32 u (u < UQ) of
+    // each are loaded before any is used; longer regions finish in a tail loop.
+    constexpr int RQ = 4, UQ = 2;
+    for (int rb0 = warp; rb0 < nreg; rb0 += (NT / 32) * RQ) {
+      uint32_t tk[RQ * UQ];
+      float sc[RQ * UQ * HPC];
+      int cnt[RQ];
+#pragma unroll
+      for (int qq = 0; qq < RQ; ++qq) {
+        const int r = rb0 + (NT / 32) * qq;
+        cnt[qq] = r < nreg ? s_cnt[r] : 0;
+        const uint32_t* rtok = ent_tok + greg(r) * CW;
+        const float* rsc = ent_sc + greg(r) * CW * nh + e0;
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) {
+          const int i = lane + 32 * u;
+          tk[qq * UQ + u] = i < cnt[qq] ? rtok[i] : 0u;
+#pragma unroll
+          for (int hh = 0; hh < HPC; ++hh) sc[(qq * UQ + u) * HPC + hh] = i < cnt[qq] ? rsc[(size_t)i * nh + hh] : 0.f;
+        }
+      }
+      keep_entries(std::integral_constant<int, RQ * UQ>{}, tk, sc);
+      // tail: regions longer than 32 UQ entries
+      for (int qq = 0; qq < RQ; ++qq) {
+        const int r = rb0 + (NT / 32) * qq;
+        for (int i0 = 32 * UQ; i0 < cnt[qq]; i0 += 32) {
+          uint32_t tk1[1] = {0u};
+          float sc1[HPC] = {};
+          const int i = i0 + lane;
+          if (i < cnt[qq]) {
+            tk1[0] = ent_tok[greg(r) * CW + i];
+#pragma unroll
+            for (int hh = 0; hh < HPC; ++hh) sc1[hh] = ent_sc[(greg(r) * CW + i) * nh + e0 + hh];
+          }
+          keep_entries(std::integral_constant<int, 1>{}, tk1, sc1);
+        }
       }
     }
   }
@@ -1100,6 +1157,11 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const int chunk = blockIdx.x;
   const int t0 = chunk * kRangeTok;
   const size_t reg = ((size_t)bg * nch + chunk) * NW + warp;
+  // kMma: one band region per (chunk, head pair) shared by the CTA's warps
+  // (positions from a shared-memory counter per pair), capacity kChunkCap
+  const size_t creg = (size_t)bg * nch + chunk;
+  constexpr int kChunkCap = NW * CW;
+  __shared__ int s_bc[2];
   // ---- prologue: every global input is requested before anything waits on
   // one (N_b, the chunk's page ids, the channel ids, the G q rows, then the
   // brackets once the sample kernel has finished), so the CTA start costs one
@@ -1120,6 +1182,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   for (int u = 0; u < (int)(sizeof(qv) / sizeof(uint4)); ++u)
     if (tid + u * kScanNT < nq16) qv[u] = __ldg(qsrc + tid + u * kScanNT);
   for (int i = tid; i < G * kWords; i += kScanNT) s_words[i] = 0u;
+  if (tid < 2) s_bc[tid] = 0;
   // the chunk's first ring stages do not depend on the sample kernel: they are
   // requested before the PDL wait (the sample kernel lets this grid launch at
   // its start), so the scan's first copies overlap the sample
@@ -1207,7 +1270,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   for (int j = 0; j < G; ++j) thv[j] = __ldcg(reinterpret_cast<const float2*>(thr) + 2 * (row0 + j) + 1);
   if (ntok == 0) {
     if (kMma) {
-      if (lane < 2) ent_cnt[reg * 2 + lane] = 0;
+      if (tid < 2) ent_cnt[creg * 2 + tid] = 0;
     } else if (lane == 0) {
       ent_cnt[reg] = 0;
     }
@@ -1248,8 +1311,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   float* c_sc = c_sc_all + warp * G * kScanCandCap;  // this warp's candidates ([p][G])
   uint16_t* c_tok = c_tok_all + warp * kScanCandCap;
   int wn = 0;   // candidates buffered by this warp (chunk-relative tokens)
-  int wc = 0;   // band entries written (kMma: of head pair 0)
-  int wc1 = 0;  // kMma: band entries of head pair 1
+  int wc = 0;   // band entries written (union format)
   // kMma: this lane's head pair p = u & 1 (phase 1); the thresholds of both pairs (phase 2)
   const int pm_r = lane >> 2, pm_u = lane & 3, pm_p = pm_u & 1;
   const float pm_fla0 = flo[0], pm_fla1 = flo[G > 1 ? 1 : 0], pm_flb0 = flo[G > 2 ? 2 : 0], pm_flb1 = flo[G > 3 ? 3 : 0];
@@ -1278,16 +1340,17 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
         const uint32_t m = (!s0 && v.x >= (p ? pm_flb0 : pm_fla0) ? 1u : 0u) |
                            (!s1 && v.y >= (p ? pm_flb1 : pm_fla1) ? 2u : 0u);
         const uint32_t b0 = __ballot_sync(0xffffffffu, m && !p), b1 = __ballot_sync(0xffffffffu, m && p);
+        int base = 0;  // lane 0: pair 0's base, lane 1: pair 1's
+        if (lane < 2 && (lane ? b1 : b0)) base = atomicAdd(&s_bc[lane], __popc(lane ? b1 : b0));
+        const int base0 = __shfl_sync(0xffffffffu, base, 0), base1 = __shfl_sync(0xffffffffu, base, 1);
         if (m) {
-          const int pos = (p ? wc1 : wc) + __popc((p ? b1 : b0) & lt_mask);
-          if (pos < CW) {
-            const size_t e = (reg * 2 + p) * CW + pos;
+          const int pos = (p ? base1 : base0) + __popc((p ? b1 : b0) & lt_mask);
+          if (pos < kChunkCap) {
+            const size_t e = (creg * 2 + p) * kChunkCap + pos;
             st_keep_u32(ent_tok + e, (uint32_t)(t0 + i) | (m << 24), pol_keep);
             st_keep_f2(reinterpret_cast<float2*>(ent_sc) + e, v, pol_keep);
           }
         }
-        wc += __popc(b0);
-        wc1 += __popc(b1);
       }
     } else {
       for (int c0 = 0; c0 < wn; c0 += 32) {
@@ -1463,10 +1526,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     if (w < nwv) st_keep_u32(fbm + (size_t)(row0 + j) * ldw + (t0 >> 5) + w, s_words[i], pol_keep);
   }
   if (kMma) {
-    if (lane == 0) {
-      ent_cnt[reg * 2 + 0] = wc;
-      ent_cnt[reg * 2 + 1] = wc1;
-    }
+    if (tid < 2) ent_cnt[creg * 2 + tid] = s_bc[tid];  // > kChunkCap: overflow (the select's slow path)
   } else if (lane == 0) {
     ent_cnt[reg] = wc;
   }
@@ -1738,7 +1798,8 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
   const bool pair = (SkMma<G, Sk>::value || SkMmaF8<G, Sk>::value) && C == 8;  // the tensor-core scan's pair regions
   // the region count table: every band region of the longest row, unless the
   // select's shared memory cannot hold it (those rows take the exact slow path)
-  int nreg_cap = nch * kScanWarps;
+  // (the pair regions' counts are read straight from global memory: no table)
+  int nreg_cap = pair ? 0 : nch * kScanWarps;
   if (sel_core_smem(1, sel_cap, C, nreg_cap) + sizeof(SelShared<kSelNT, 1>) + 1024 > 227 * 1024) nreg_cap = 0;
   SelArgs sa{q, geo.kv_dtype, sk, skc.channel_ids, C, kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages,
              geo.Hkv, bud.dev(), w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld,
