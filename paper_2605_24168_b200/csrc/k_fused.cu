@@ -1230,10 +1230,16 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
       } else if (C8) {
         const int* sp = s_pages + (s * kScanStageTok8 >> 4) + ((tid * kTpc) >> 4);
         if ((s + 1) * kScanStageTok8 <= ntok) {  // full stage: plain copies
+          // every page id is read before the first copy is issued: the copies then
+          // issue back to back (no shared-memory load between two LDGSTS)
+          constexpr int kU = kScanStageTok8 / kScanNT / kTpc;
+          uint32_t pgu[kU];
 #pragma unroll
-          for (int u = 0; u < kScanStageTok8 / kScanNT / kTpc; ++u) {
+          for (int u = 0; u < kU; ++u) pgu[u] = (uint32_t)sp[u * (kScanNT * kTpc >> 4)];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
             const uint32_t d = smem_u32(st + (size_t)(tid + u * kScanNT) * 16);
-            const char* src = tb + (size_t)(uint32_t)sp[u * (kScanNT * kTpc >> 4)] * page_bytes;
+            const char* src = tb + (size_t)pgu[u] * page_bytes;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
           }
         } else {  // the range's tail: only the pages that exist (rows >= N are masked)
