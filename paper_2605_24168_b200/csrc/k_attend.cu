@@ -18,6 +18,9 @@
 
 #include "sd_common.cuh"
 #include "sd_internal.h"
+#include "sd_merge.cuh"
+
+static_assert(sd::kMergeStride == sd::kPartStride, "merge helper and partial layout agree");
 
 namespace sd {
 
@@ -158,7 +161,6 @@ __global__ void __launch_bounds__(kAttThreads) attend_list_kernel(
 // Up to kMergeRegSplits splits (N <= 128K at 8192 tokens per split) take a
 // register path with a single round of loads; more splits use shared memory.
 // ---------------------------------------------------------------------------
-constexpr int kMergeRegSplits = 16;
 __global__ void __launch_bounds__(128) merge_parts_kernel(const float* __restrict__ part, int splits,
                                                           void* __restrict__ out, int out_dtype,
                                                           float* __restrict__ lse) {
@@ -169,30 +171,7 @@ __global__ void __launch_bounds__(128) merge_parts_kernel(const float* __restric
   pdl_wait();  // no-op unless launched as a programmatic dependent
   const float* p = part + (size_t)row * splits * kPartStride;
   if (splits <= kMergeRegSplits) {
-    // every split's (m, l, o[d]) in registers after one round of independent
-    // loads; merged in split order (deterministic)
-    float mv[kMergeRegSplits], lv[kMergeRegSplits], ov[kMergeRegSplits];
-    float M = -INFINITY;
-#pragma unroll
-    for (int s = 0; s < kMergeRegSplits; ++s) {
-      const bool in = s < splits;
-      mv[s] = in ? __ldcg(p + s * kPartStride) : -INFINITY;
-      lv[s] = in ? __ldcg(p + s * kPartStride + 1) : 0.f;
-      ov[s] = in ? __ldcg(p + s * kPartStride + 2 + d) : 0.f;
-    }
-#pragma unroll
-    for (int s = 0; s < kMergeRegSplits; ++s) M = fmaxf(M, mv[s]);
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int s = 0; s < kMergeRegSplits; ++s) {
-        const float c = mv[s] == -INFINITY ? 0.f : exp2f(mv[s] - M);
-        L = fmaf(lv[s], c, L);
-        O = fmaf(ov[s], c, O);
-      }
-    }
-    store_out(out, out_dtype, (size_t)row * kD + d, L > 0.f ? O / L : 0.f);
-    if (lse && d == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+    merge_row_regs(part, splits, row, d, out, out_dtype, lse);
     return;
   }
   float mv[4], lv[4], M = -INFINITY;

@@ -78,6 +78,22 @@ constexpr int kTieCap = 2048;
 #define SD_SEL_UQ 6  // select, pair regions: entries per lane requested with the region count
 #endif
 
+// The two sample order statistics that bracket the k-th key (k_fused.cu header):
+// r_lo = ceil(k f + z sqrt(k f (1-f)) + 1), r_hi = floor(k f - z sqrt(...)),
+// f = n_s / N; the whole row sampled: both = k.  fp32 (the bracket is a filter
+// the select verifies, so only determinism matters; fp64 here cost ~200
+// instructions per thread of the sample kernel).
+__device__ __forceinline__ void sample_ranks(int k, int n_s, int N, int* r_lo, int* r_hi) {
+  if (n_s >= N) {
+    *r_lo = *r_hi = k;
+    return;
+  }
+  const float f = __fdiv_rn((float)n_s, (float)N);
+  const float mu = (float)k * f, sd = sqrtf(mu * (1.f - f));
+  *r_lo = (int)ceilf(mu + kBracketZ * sd + 1.f);
+  *r_hi = (int)floorf(mu - kBracketZ * sd);
+}
+
 __device__ __forceinline__ float load_q_elem(const void* q, int q_dtype, size_t e) {
   return q_dtype == SD_F32 ? reinterpret_cast<const float*>(q)[e]
                            : bf_lo(reinterpret_cast<const uint16_t*>(q)[e]);
@@ -341,14 +357,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_kernel(
   const int last_sampled = (ns_pages - 1) * spg;
   const int n_s = n_slots - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
   int r_lo, r_hi;
-  if (n_s >= N) {
-    r_lo = r_hi = k;
-  } else {
-    const double f = (double)n_s / (double)N;
-    const double mu = (double)k * f, sd = sqrt((double)k * f * (1.0 - f));
-    r_lo = (int)ceil(mu + kBracketZ * sd + 1.0);
-    r_hi = (int)floor(mu - kBracketZ * sd);
-  }
+  sample_ranks(k, n_s, N, &r_lo, &r_hi);
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
   __syncthreads();
   hist_group_sums<NT>(hist1, G, s_grp);
@@ -510,14 +519,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_mma_kernel(
   const int last_sampled = (ns_pages - 1) * spg;
   const int n_s = ns_pages * 16 - ((last_sampled == npg - 1) ? (npg * 16 - N) : 0);
   int r_lo, r_hi;
-  if (n_s >= N) {
-    r_lo = r_hi = k;
-  } else {
-    const double f = (double)n_s / (double)N;
-    const double mu = (double)k * f, sd = sqrt((double)k * f * (1.0 - f));
-    r_lo = (int)ceil(mu + kBracketZ * sd + 1.0);
-    r_hi = (int)floor(mu - kBracketZ * sd);
-  }
+  sample_ranks(k, n_s, N, &r_lo, &r_hi);
   const uint32_t ra = (uint32_t)min(r_lo, n_s), rb = (uint32_t)max(r_hi, 1);
   const uint32_t kmin = 4u * ra <= (uint32_t)n_s ? 0x80000000u : 0u;  // level-1 key floor
   const int hsel = 2 * (uu & 1) - j0;  // this lane's first head, relative to the CTA's
