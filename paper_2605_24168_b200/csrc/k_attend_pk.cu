@@ -121,6 +121,12 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifdef SD_ATTEND_TRACE
+// debug builds only (-DSD_ATTEND_TRACE, scripts/attend_trace.py): per CTA
+// {start, first unit ready, end, units} in %globaltimer ns
+__device__ unsigned long long g_attend_trace[1024][4];
+#endif
+
 template <int G>
 __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
     const uint16_t* __restrict__ q, const char* __restrict__ kp, const char* __restrict__ vp,
@@ -149,6 +155,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
     return;
   }
   pdl_wait();  // selection bitmaps come from sbs_select_kernel
+#ifdef SD_ATTEND_TRACE
+  if (tid == 0) g_attend_trace[blockIdx.x][0] = globaltimer_ns();
+#endif
 
   if (warp >= kPkWarps) {
     // =================================================================== producers
@@ -338,6 +347,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) attend_union_ws_kernel(
       const int buf = u & 1;
       mbar_wait(&sm.ready[buf], (uint32_t)(u >> 1) & 1u);
       const int it_c = sm.u_it[buf];
+#ifdef SD_ATTEND_TRACE
+      if (tid == 0 && u == 0) g_attend_trace[blockIdx.x][1] = globaltimer_ns();
+      if (tid == 0 && it_c >= n_items) {
+        g_attend_trace[blockIdx.x][2] = globaltimer_ns();
+        g_attend_trace[blockIdx.x][3] = (unsigned long long)u;
+      }
+#endif
       if (it_c >= n_items) break;
       const int r0_c = sm.u_r0[buf], nrows_c = sm.u_nrows[buf], last_c = sm.u_last[buf];
       if (r0_c == 0) {
@@ -585,3 +601,9 @@ cudaError_t launch_attend_union_pk(const Geo& g, const sd_paged_kv& kv, const vo
 }
 
 }  // namespace sd
+
+#ifdef SD_ATTEND_TRACE
+extern "C" int sd_debug_attend_trace(unsigned long long* host, int n_ctas) {
+  return (int)cudaMemcpyFromSymbol(host, sd::g_attend_trace, sizeof(unsigned long long) * 4 * n_ctas);
+}
+#endif
