@@ -1210,10 +1210,13 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   constexpr int kRowB = 8 * Sk::kBytes;  // C8: one token's sketch row (16 B bf16, 8 B fp8)
   constexpr int kTpc = 16 / kRowB;       // C8: tokens per 16-B copy
   const char* tb = skb + ((size_t)g * kPS + ((tid * kTpc) & 15)) * kRowB;
+  // (one opaque 64-bit base: each copy address is then a single IMAD.WIDE.U32)
+  asm("mov.b64 %0, %0;" : "+l"(tb));
   const uint32_t page_bytes = (uint32_t)Hkv * kPS * kRowB;
-  auto issue = [&](int s) {
+  // stage s into ring slot `slot` (== s % kScanStages, kept by the caller)
+  auto issue = [&](int s, int slot) {
     if (s < nst) {
-      unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
+      unsigned char* st = ring + (size_t)slot * stage_bytes;
       if (C8 && SkMmaF8<G, Sk>::value) {
         // fp8 rows, tensor-core path: warp w copies its own 4 blocks of 32 tokens
         // (stage tokens 256 j + 32 w + [0, 32)), 2 tokens per 16-B copy, so a warp
@@ -1269,7 +1272,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int s = 0; s < kScanStages - 1; ++s) issue(s);
+  for (int s = 0; s < kScanStages - 1; ++s) issue(s, s);
   pdl_wait();  // the bracket comes from the sample kernel
   float2 thv[G];  // {flo, fsure} per head, converted by the sample kernel
   // (written by the PDL primary while this grid may already run: coherent
@@ -1326,6 +1329,9 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
   const float pm_fsa0 = fsure[0], pm_fsa1 = fsure[G > 1 ? 1 : 0], pm_fsb0 = fsure[G > 2 ? 2 : 0],
               pm_fsb1 = fsure[G > 3 ? 3 : 0];
   const float pm_fl0 = pm_p ? pm_flb0 : pm_fla0, pm_fl1 = pm_p ? pm_flb1 : pm_fla1;
+  // candidate code of token tA = blk + pm_r + 16 (pm_u >> 1) (< 2^15, no carry into bit 15):
+  // (stage-relative block start) + this lane's constant (offset | pair << 15)
+  const int pm_lc = (warp * 32 + pm_r + ((pm_u >> 1) << 4)) | (pm_p << 15);
   float2* pm_c2 = reinterpret_cast<float2*>(c_sc_all) + warp * 2 * kScanCandCap;  // [2 * kScanCandCap]
   uint16_t* pm_ct = c_tok_all + warp * 2 * kScanCandCap;
   const uint32_t pm_c2_s = smem_u32(pm_c2), pm_ct_s = smem_u32(pm_ct);  // shared-window addresses
@@ -1389,16 +1395,19 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     wn = 0;
   };
 
+  const uint32_t ring_s = smem_u32(ring);
+  int slot = 0;  // s % kScanStages
   for (int s = 0; s < nst; ++s) {
-    issue(s + kScanStages - 1);
+    const int slot_prev = slot == 0 ? kScanStages - 1 : slot - 1;  // (s + kScanStages - 1) % kScanStages
+    issue(s + kScanStages - 1, slot_prev);
     asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
     // bf16 rows at C = 8: thread tid copies tokens tid + 256 u of a stage, which
     // are exactly the 32-token blocks its warp scores, so a warp only waits for
     // its own lanes' copies (no CTA barrier per stage); otherwise the CTA syncs
     if constexpr (kWarpLocal) __syncwarp();
     else __syncthreads();
-    const unsigned char* st = ring + (size_t)(s % kScanStages) * stage_bytes;
-    const uint32_t st_w = smem_u32(st) + (uint32_t)warp * 32u * 16u;  // this warp's first block of the stage
+    const unsigned char* st = ring + (size_t)slot * stage_bytes;
+    const uint32_t st_w = ring_s + (uint32_t)(slot * stage_bytes) + (uint32_t)warp * 32u * 16u;  // this warp's first block
     const int cb = s * stage_tok;                   // chunk-relative first token of the stage
     const int lim = min(stage_tok, ntok - cb);      // valid tokens of this stage
     const int tbase = t0 + cb;                      // first token of the stage
@@ -1455,10 +1464,11 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
             const uint32_t bA = __ballot_sync(0xffffffffu, cA), bB = __ballot_sync(0xffffffffu, cB);
             const int nA = __popc(bA);
             const int pA = wn + __popc(bA & lt_mask), pB = wn + nA + __popc(bB & lt_mask);
+            const int code0 = cb + i0 + h * kScanNT + pm_lc;  // == (cb + tA) | pm_p << 15
             st_cand_pred(cA, pm_c2_s + 8u * (uint32_t)pA, d[h][0], d[h][1], pm_ct_s + 2u * (uint32_t)pA,
-                         (uint16_t)((cb + tA) | (pm_p << 15)));
+                         (uint16_t)code0);
             st_cand_pred(cB, pm_c2_s + 8u * (uint32_t)pB, d[h][2], d[h][3], pm_ct_s + 2u * (uint32_t)pB,
-                         (uint16_t)((cb + tB) | (pm_p << 15)));
+                         (uint16_t)(code0 + 8));
             wn += nA + __popc(bB);
           }
         }
@@ -1522,6 +1532,7 @@ __global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
     // every lane (warp-local staging) / warp is done with the slot before issue() refills it
     if constexpr (kWarpLocal) __syncwarp();
     else __syncthreads();
+    slot = slot == kScanStages - 1 ? 0 : slot + 1;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   flush();
