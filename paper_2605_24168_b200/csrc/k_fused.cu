@@ -69,8 +69,15 @@ __host__ __device__ __forceinline__ int sample_rounds(int N) {
 }
 constexpr int kScanNT = 256;               // 8 warps
 constexpr int kScanStageTok8 = 1024;       // tokens per ring stage at C = 8 (16 KB)
-constexpr int kScanStages = 3;
-constexpr int kScanCandCap = kScanStageTok8 / 8;    // candidates per warp per stage (<= its tokens)
+// Two scan shapes (template NS = ring stages).  NS = 2 with 96-entry candidate
+// buffers keeps the CTA at ~53 KB of shared memory and 64 registers: 4 CTAs (32
+// warps) per SM, for grids of more than one 3-CTA/SM wave — the scan is latency-
+// bound per warp, so occupancy beats ring depth there (cfg3: 3 stages at 3 CTAs/SM
+// 59.6 us, 4-5 stages at 2 CTAs/SM 65 us, 2 stages at 4 CTAs/SM 57.9 us).  Smaller
+// grids (cfg2, cfg4 turn 0: a partial wave) keep NS = 3 at 3 CTAs/SM, whose deeper
+// ring serves a lone CTA better (cfg2 S = 50: 59.4 vs 63.3 us).
+__host__ __device__ constexpr int scan_cand_cap(int ns) { return ns == 2 ? 96 : 128; }
+__host__ __device__ constexpr int scan_min_blocks(int ns, int g) { return ns == 2 && g < 8 ? 4 : 3; }
 constexpr int kSelNT = 256;           // 4 CTAs per SM: B*Hq = 512 rows in one wave
 constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
 constexpr int kTieCap = 2048;
@@ -1123,12 +1130,14 @@ __device__ __forceinline__ void load_scores(float (&sc)[G], const float* src) {
   }
 }
 
-template <int G, bool C8, class Sk>
-__global__ void __launch_bounds__(kScanNT, 3) sbs_scan_kernel(
+template <int G, bool C8, class Sk, int NS>
+__global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
     int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud) {
+  constexpr int kScanStages = NS;                    // ring stages
+  constexpr int kScanCandCap = scan_cand_cap(NS);    // candidate buffer per warp (x2 entries on the MMA path)
   constexpr int NW = kScanNT / 32;
   static_assert(NW == kScanWarps, "one band region per scan warp");
   constexpr int CW = band_region_cap(G);
@@ -1824,12 +1833,15 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
              geo.Hkv, bud.dev(), w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, nch, w.fbm, w.ldw, w.scratch, w.ld,
              w.counts_out, w.force_fallback, w.err, sel_cap, nreg_cap};
   {
-    const size_t smem = (size_t)kScanStages * kScanStageTok8 * 16 +
+    // 4 CTAs/SM (NS = 2) when the grid exceeds one 3-CTA/SM wave
+    const int ns = (size_t)nch * BG > (size_t)3 * geo.sms ? 2 : 3;
+    const size_t smem = (size_t)ns * kScanStageTok8 * 16 +
                         sizeof(float) * G * C + sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * (kRangeTok / 32) +
-                        (sizeof(float) * G + 2 * sizeof(uint16_t)) * kScanWarps * kScanCandCap;
+                        (sizeof(float) * G + 2 * sizeof(uint16_t)) * kScanWarps * scan_cand_cap(ns);
     dim3 grid(nch, BG);
     // the fp8 sketch is C = 8 only (host-checked): no generic-C fp8 variant
-    auto kern = C == 8 ? sbs_scan_kernel<G, true, Sk> : sbs_scan_kernel<G, false, SkBf16>;
+    auto kern = C == 8 ? (ns == 2 ? sbs_scan_kernel<G, true, Sk, 2> : sbs_scan_kernel<G, true, Sk, 3>)
+                       : (ns == 2 ? sbs_scan_kernel<G, false, SkBf16, 2> : sbs_scan_kernel<G, false, SkBf16, 3>);
     e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
