@@ -57,9 +57,12 @@ struct WsLayout {
   // fused path (sample-bracket select, sd_sbs.cuh)
   int nrange = 0, ldw = 0;
   size_t thr = 0;            // uint32 [B*Hq][4]: bracket keys lo, hi; float thresholds flo, fsure
-  size_t ent_tok = 0;        // uint32 token | head mask << 24  [B*Hkv][nrange * 8][cap]  (union band)
-  size_t ent_sc = 0;         // float scores [B*Hkv][nrange * 8][cap][G]
-  size_t ent_cnt = 0;        // int32 [B*Hkv][nrange * 8] entry counts (> cap: overflow)
+  // band entries (sd_sbs.cuh): union format [B*Hkv][nrange * 8 warps][cap] with G
+  // scores each, or (G = 4 tensor-core scan) [B*Hkv][nrange][2 pairs][8 cap] with
+  // 2 scores each -- the same bytes
+  size_t ent_tok = 0;        // uint32 token | head mask << 24
+  size_t ent_sc = 0;         // float scores
+  size_t ent_cnt = 0;        // int32 entry count per region (> capacity: overflow -> slow path)
   size_t fbm = 0;            // uint32 [B*Hq][ldw] selection bitmap
   size_t ctr = 0;            // int32 [B*Hkv + 1] last-CTA merge counters + work counter (zero between calls)
   size_t total = 0;

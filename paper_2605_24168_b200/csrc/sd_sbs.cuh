@@ -7,8 +7,12 @@
 //                                    thresholds for the scan        (sbs_sample_kernel)
 //   fbm[row][t / 32] bit t = key(s_t) > hi after sbs_scan_kernel (sure tokens),
 //                          = t is in the exact top-k_b after sbs_select_kernel
-//   band entries (lo <= key <= hi for some head of the group): per (b, g,
-//   8192-token chunk, scan warp) region, token | head mask << 24 and G scores
+//   band entries (lo <= key <= hi for some head of the group): token | head
+//   mask << 24 and the scores.  Tensor-core scan (G = 4, C = 8): one region per
+//   (b, g, 8192-token chunk, head pair p) of capacity 8 * band_region_cap(4),
+//   filled by the scan CTA's 8 warps through a shared-memory position counter,
+//   the pair's 2 scores per entry (mask bits 2p, 2p + 1).  Otherwise: one region
+//   per (b, g, chunk, scan warp) of capacity band_region_cap(G), G scores per entry.
 // where key() is the order-preserving uint32 map of the fp32 indexer score
 // (sd_common.cuh score_key).  A gather-attend CTA owning tokens [T0, T1) of
 // (b, g) ORs the G heads' fbm words of its range into the ascending GQA union
