@@ -1130,6 +1130,10 @@ __device__ __forceinline__ void load_scores(float (&sc)[G], const float* src) {
   }
 }
 
+#ifdef SD_SCAN_TRACE
+// debug builds only (-DSD_SCAN_TRACE): per scan CTA {after PDL wait, end} in %globaltimer ns
+__device__ unsigned long long g_scan_trace[8192][2];
+#endif
 template <int G, bool C8, class Sk, int NS>
 __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kernel(
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
@@ -1283,6 +1287,9 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
 #pragma unroll
   for (int s = 0; s < kScanStages - 1; ++s) issue(s, s);
   pdl_wait();  // the bracket comes from the sample kernel
+#ifdef SD_SCAN_TRACE
+  if (tid == 0) g_scan_trace[blockIdx.y * gridDim.x + blockIdx.x][0] = globaltimer_ns();
+#endif
   float2 thv[G];  // {flo, fsure} per head, converted by the sample kernel
   // (written by the PDL primary while this grid may already run: coherent
   // L2 loads, not the read-only path)
@@ -1558,6 +1565,9 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
   } else if (lane == 0) {
     ent_cnt[reg] = wc;
   }
+#ifdef SD_SCAN_TRACE
+  if (tid == 0) g_scan_trace[blockIdx.y * gridDim.x + blockIdx.x][1] = globaltimer_ns();
+#endif
   pdl_launch_dependents();
 }
 
@@ -1898,3 +1908,9 @@ cudaError_t launch_sbs_select(const Geo& g, const sd_paged_kv& kv, const sd_sket
 }
 
 }  // namespace sd
+
+#ifdef SD_SCAN_TRACE
+extern "C" int sd_debug_scan_trace(unsigned long long* host, int n_ctas) {
+  return (int)cudaMemcpyFromSymbol(host, sd::g_scan_trace, sizeof(unsigned long long) * 2 * n_ctas);
+}
+#endif
