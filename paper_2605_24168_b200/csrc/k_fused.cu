@@ -81,6 +81,9 @@ __host__ __device__ constexpr int scan_min_blocks(int ns, int g) { return ns == 
 constexpr int kSelNT = 256;           // 4 CTAs per SM: B*Hq = 512 rows in one wave
 constexpr int kSelCap = 24576;             // band entries cached per row (keys + tokens: 192 KB)
 constexpr int kTieCap = 2048;
+#ifndef SD_SCAN_HALF
+#define SD_SCAN_HALF 2  // half-chunk scan CTAs at the end: (this * SMs) / 2 items (4: 195.3, 2: 194.1, 0: 195.1 us)
+#endif
 #ifndef SD_SEL_UQ
 #define SD_SEL_UQ 6  // select, pair regions: entries per lane requested with the region count
 #endif
@@ -802,9 +805,24 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
     // counts, the entries and the sure-count words arrive in one memory round
     // trip; entries past the count are dropped, longer regions finish in rounds
     // of kUT * 32.
-    constexpr int kCWC = NW * CW;
+    constexpr int kCWC = NW * CW, kSub = kCWC / 2;  // chunk region, its two sub-regions
     constexpr int kUQ = SD_SEL_UQ, kUT = 4;
     const int nchr = (N + kRangeTok - 1) / kRangeTok;
+    // kUT-entry-per-lane rounds over entries [i0, cnt) of a sub-region
+    auto keep_rest = [&](const uint32_t* rtok, const float* rsc, int i0, int cnt) {
+      for (; i0 < cnt; i0 += 32 * kUT) {
+        uint32_t tk1[kUT];
+        float sc1[kUT * HPC];
+#pragma unroll
+        for (int u = 0; u < kUT; ++u) {
+          const int i = i0 + lane + 32 * u;
+          tk1[u] = i < cnt ? rtok[i] : 0u;
+#pragma unroll
+          for (int hh = 0; hh < HPC; ++hh) sc1[u * HPC + hh] = i < cnt ? rsc[(size_t)i * 2 + hh] : 0.f;
+        }
+        keep_entries(std::integral_constant<int, kUT>{}, tk1, sc1);
+      }
+    };
     for (int c0 = warp; c0 < nchr; c0 += NT / 32) {
       const size_t cr = ((size_t)bg * nch + c0) * 2 + sub;
       const uint32_t* rtok = ent_tok + cr * kCWC;
@@ -823,28 +841,18 @@ __device__ __forceinline__ void select_core(const SelArgs& a, int row_base, unsi
           sc[u] = rsc[(size_t)i * 2];
         }
       }
-      int cnt = ent_cnt[cr];
+      int cnt = ent_cnt[cr * 2], cnt1 = ent_cnt[cr * 2 + 1];  // sub-region 1: a second half-chunk CTA
       if (c0 == warp) sure_count();  // (first pass only) its loads overlap the entries'
-      if (cnt > kCWC) {  // region overflow: exact slow path
+      if (cnt > kSub || cnt1 > kSub) {  // region overflow: exact slow path
         for (int hh = 0; hh < HPC; ++hh) s_fb[hh] = 1;
-        cnt = 0;
+        cnt = cnt1 = 0;
       }
 #pragma unroll
       for (int u = 0; u < kUQ; ++u)
         if (lane + 32 * u >= cnt) tk[u] = 0u;
       keep_entries(std::integral_constant<int, kUQ>{}, tk, sc);
-      for (int i0 = 32 * kUQ; i0 < cnt; i0 += 32 * kUT) {
-        uint32_t tk1[kUT];
-        float sc1[kUT * HPC];
-#pragma unroll
-        for (int u = 0; u < kUT; ++u) {
-          const int i = i0 + lane + 32 * u;
-          tk1[u] = i < cnt ? rtok[i] : 0u;
-#pragma unroll
-          for (int hh = 0; hh < HPC; ++hh) sc1[u * HPC + hh] = i < cnt ? rsc[(size_t)i * 2 + hh] : 0.f;
-        }
-        keep_entries(std::integral_constant<int, kUT>{}, tk1, sc1);
-      }
+      keep_rest(rtok, rsc, 32 * kUQ, cnt);
+      keep_rest(rtok + kSub, rsc + (size_t)kSub * 2, 0, cnt1);
     }
     if (warp >= nchr) sure_count();
   } else {
@@ -1139,7 +1147,7 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
     const void* __restrict__ q, int q_dtype, const char* __restrict__ skb, const int* __restrict__ channel_ids,
     int C, const int* __restrict__ page_table, const int* __restrict__ seq_lens, int max_len, int max_pages, int Hkv,
     const uint32_t* __restrict__ thr, uint32_t* __restrict__ ent_tok, float* __restrict__ ent_sc,
-    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud) {
+    int* __restrict__ ent_cnt, uint32_t* __restrict__ fbm, int ldw, int nch, BudgetDev bud, int n_half) {
   constexpr int kScanStages = NS;                    // ring stages
   constexpr int kScanCandCap = scan_cand_cap(NS);    // candidate buffer per warp (x2 entries on the MMA path)
   constexpr int NW = kScanNT / 32;
@@ -1165,17 +1173,30 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
   float* c_sc_all = reinterpret_cast<float*>(s_words + G * kWords);                       // [NW][kScanCandCap][G]
   uint16_t* c_tok_all = reinterpret_cast<uint16_t*>(c_sc_all + NW * G * kScanCandCap);    // [NW][2 kScanCandCap]
 
-  const int bg = blockIdx.y, b = bg / Hkv, g = bg - b * Hkv;
+  // 1-D grid in (b, g)-major, chunk-minor order; the last n_half items (the
+  // final wave, kMma path only) run as two CTAs of half a chunk each, so the
+  // scan's tail is half as long
+  const int n_items = (int)gridDim.x - n_half;  // items = B * Hkv * nch
+  const int nfull = n_items - n_half;
+  int item = blockIdx.x, half = -1;
+  if (item >= nfull) {
+    half = (item - nfull) & 1;
+    item = nfull + ((item - nfull) >> 1);
+  }
+  const int bg = item / nch, b = bg / Hkv, g = bg - b * Hkv;
   const int Hq = Hkv * G;
   const int row0 = b * Hq + g * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int chunk = blockIdx.x;
-  const int t0 = chunk * kRangeTok;
+  const int chunk = item - bg * nch;
+  const int t0 = chunk * kRangeTok + (half == 1 ? kRangeTok / 2 : 0);
+  const int len = half < 0 ? kRangeTok : kRangeTok / 2;  // tokens of this CTA
   const size_t reg = ((size_t)bg * nch + chunk) * NW + warp;
   // kMma: one band region per (chunk, head pair) shared by the CTA's warps
-  // (positions from a shared-memory counter per pair), capacity kChunkCap
+  // (positions from a shared-memory counter per pair), two sub-regions of
+  // kSubCap (sub-region 1: the second half-chunk CTA), a count per sub-region
   const size_t creg = (size_t)bg * nch + chunk;
-  constexpr int kChunkCap = NW * CW;
+  constexpr int kChunkCap = NW * CW, kSubCap = kChunkCap / 2;
+  const int sr = half == 1 ? 1 : 0;
   __shared__ int s_bc[2];
   // ---- prologue: every global input is requested before anything waits on
   // one (N_b, the chunk's page ids, the channel ids, the G q rows, then the
@@ -1184,7 +1205,7 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
   const int qb = q_dtype == SD_F32 ? 4 : 2;
   const int N = max(0, seq_len_dev(seq_lens, b, max_len));  // out of range: an empty row
   const int* pt = page_table + (size_t)b * max_pages + (t0 >> 4);
-  const int np_max = min(kRangeTok / 16, max_pages - (t0 >> 4));  // page ids past N_b are never used
+  const int np_max = min(len / 16, max_pages - (t0 >> 4));  // page ids past N_b are never used
   constexpr int kPgPerThr = kRangeTok / 16 / kScanNT;
   int pgv[kPgPerThr];
 #pragma unroll
@@ -1201,7 +1222,7 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
   // the chunk's first ring stages do not depend on the sample kernel: they are
   // requested before the PDL wait (the sample kernel lets this grid launch at
   // its start), so the scan's first copies overlap the sample
-  const int ntok = max(0, min(N - t0, kRangeTok));
+  const int ntok = max(0, min(N - t0, len));
   // the q rows and channel ids are staged in the candidate area (unused until phase 1)
   unsigned char* s_qrow = reinterpret_cast<unsigned char*>(c_sc_all);        // [G][kD] q dtype
   int* s_ch = reinterpret_cast<int*>(s_qrow + (size_t)G * kD * 4);            // [C]
@@ -1297,7 +1318,8 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
   for (int j = 0; j < G; ++j) thv[j] = __ldcg(reinterpret_cast<const float2*>(thr) + 2 * (row0 + j) + 1);
   if (ntok == 0) {
     if (kMma) {
-      if (tid < 2) ent_cnt[creg * 2 + tid] = 0;
+      if (tid < 2) ent_cnt[(creg * 2 + tid) * 2 + sr] = 0;
+      if (half < 0 && tid < 2) ent_cnt[(creg * 2 + tid) * 2 + 1] = 0;
     } else if (lane == 0) {
       ent_cnt[reg] = 0;
     }
@@ -1375,8 +1397,8 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
         const int base0 = __shfl_sync(0xffffffffu, base, 0), base1 = __shfl_sync(0xffffffffu, base, 1);
         if (m) {
           const int pos = (p ? base1 : base0) + __popc((p ? b1 : b0) & lt_mask);
-          if (pos < kChunkCap) {
-            const size_t e = (creg * 2 + p) * kChunkCap + pos;
+          if (pos < kSubCap) {
+            const size_t e = (creg * 2 + p) * kChunkCap + sr * kSubCap + pos;
             st_keep_u32(ent_tok + e, (uint32_t)(t0 + i) | (m << 24), pol_keep);
             st_keep_f2(reinterpret_cast<float2*>(ent_sc) + e, v, pol_keep);
           }
@@ -1561,7 +1583,8 @@ __global__ void __launch_bounds__(kScanNT, scan_min_blocks(NS, G)) sbs_scan_kern
     if (w < nwv) st_keep_u32(fbm + (size_t)(row0 + j) * ldw + (t0 >> 5) + w, s_words[i], pol_keep);
   }
   if (kMma) {
-    if (tid < 2) ent_cnt[creg * 2 + tid] = s_bc[tid];  // > kChunkCap: overflow (the select's slow path)
+    if (tid < 2) ent_cnt[(creg * 2 + tid) * 2 + sr] = s_bc[tid];  // > kSubCap: overflow (the select's slow path)
+    if (half < 0 && tid < 2) ent_cnt[(creg * 2 + tid) * 2 + 1] = 0;  // a whole chunk: empty second sub-region
   } else if (lane == 0) {
     ent_cnt[reg] = wc;
   }
@@ -1848,7 +1871,11 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     const size_t smem = (size_t)ns * kScanStageTok8 * 16 +
                         sizeof(float) * G * C + sizeof(int) * (kRangeTok / 16) + sizeof(uint32_t) * G * (kRangeTok / 32) +
                         (sizeof(float) * G + 2 * sizeof(uint16_t)) * kScanWarps * scan_cand_cap(ns);
-    dim3 grid(nch, BG);
+    // the final 4-CTA/SM wave's worth of items as half-chunk CTAs (tensor-core
+    // pair-region path only): the scan's tail is half as long
+    const int n_items = nch * BG;
+    const int n_half = (pair && ns == 2) ? std::min(n_items / 4, (SD_SCAN_HALF * geo.sms) / 2) : 0;
+    dim3 grid(n_items + n_half);
     // the fp8 sketch is C = 8 only (host-checked): no generic-C fp8 variant
     auto kern = C == 8 ? (ns == 2 ? sbs_scan_kernel<G, true, Sk, 2> : sbs_scan_kernel<G, true, Sk, 3>)
                        : (ns == 2 ? sbs_scan_kernel<G, false, SkBf16, 2> : sbs_scan_kernel<G, false, SkBf16, 3>);
@@ -1857,7 +1884,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     e = launch_pdl(kern, grid, dim3(kScanNT), smem, st, true, q, geo.kv_dtype,
                    reinterpret_cast<const char*>(skc.pages), skc.channel_ids, C, kv.page_table, kv.seq_lens,
                    geo.max_seq_len, geo.max_pages, geo.Hkv, (const uint32_t*)w.thr, w.ent_tok, w.ent_sc, w.ent_cnt, w.fbm, w.ldw, nch,
-                   bud.dev());
+                   bud.dev(), n_half);
     if (e != cudaSuccess) return e;
     if (w.ev) cudaEventRecord(w.ev[1], st);
   }

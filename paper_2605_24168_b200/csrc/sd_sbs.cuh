@@ -11,7 +11,9 @@
 //   mask << 24 and the scores.  Tensor-core scan (G = 4, C = 8): one region per
 //   (b, g, 8192-token chunk, head pair p) of capacity 8 * band_region_cap(4),
 //   filled by the scan CTA's 8 warps through a shared-memory position counter,
-//   the pair's 2 scores per entry (mask bits 2p, 2p + 1).  Otherwise: one region
+//   the pair's 2 scores per entry (mask bits 2p, 2p + 1); its two halves are
+//   sub-regions with a count each (the scan's last items run as two half-chunk
+//   CTAs, one per sub-region; a whole-chunk CTA fills sub-region 0).  Otherwise: one region
 //   per (b, g, chunk, scan warp) of capacity band_region_cap(G), G scores per entry.
 // where key() is the order-preserving uint32 map of the fp32 indexer score
 // (sd_common.cuh score_key).  A gather-attend CTA owning tokens [T0, T1) of
