@@ -359,6 +359,32 @@ def test_fused_selection_is_exact_topk_of_gpu_scores(cuda_lib, Hq, Hkv, dist, sk
             assert np.array_equal(idx[b, h, :k], ref), (b, h)
 
 
+@pytest.mark.parametrize("dist", ["iid", "dup"])
+def test_fused_exact_topk_large_grid_ragged(cuda_lib, dist):
+    """The scan's 4-CTA/SM shape (grids above one 3-CTA/SM wave) and its half-chunk
+    CTAs in the last wave (two band sub-regions per chunk region, k_fused.cu):
+    B = 16 ragged rows (a row ending inside the second half of a split chunk, one
+    ending on a half boundary, short rows), every row's selection equal bit for bit
+    to oracle.topk_select of the GPU's own fp32 scores (S:200 ties)."""
+    sd = cuda_lib
+    lens = [70001, 5000, 65536, 61440, 69000, 4097, 33333, 70001,
+            50000, 8192, 12289, 69632, 45056 + 4095, 70000, 61441, 57345]
+    case = _dev(workloads.make_case(len(lens), 32, 8, lens, seed=91, dist=dist, n_needles=64))
+    kv, sk = _kv(sd, case)
+    sd.clear_device_error()
+    _, _, idx, cnt = sd.sparse_decode_fused(case.q, kv, sk, S=50.0, scale=SCALE, return_idx=True)
+    assert sd.read_device_error() == 0
+    assert sd.read_stats()["fallback_rows"] <= 2  # (deterministic inputs; the fast path is what this covers)
+    sc = sd.sparse_index_score(case.q, kv, sk).cpu().numpy()
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for b, N in enumerate(lens):
+        k = oracle.budget_k(50.0, N)
+        for h in range(32):
+            ref = oracle.topk_select(sc[b, h, :N].astype(np.float64), k)
+            assert cnt[b, h] == k
+            assert np.array_equal(idx[b, h, :k], ref), (b, h)
+
+
 def test_seq_len_above_max_seq_len_is_reported(cuda_lib):
     """sdattn.h: N_b > max_seq_len (or < 1) is a device error (SD_DEVERR_SEQLEN);
     the row reads as empty (out = 0, lse = -inf) and nothing else is touched:
