@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_kernel(
   // the scan grid may launch now: its CTAs stage their page ids and first
   // sketch stages, then wait (griddepcontrol.wait) for this grid to complete
   pdl_launch_dependents();
+  pdl_wait();  // (PDL-launched: the preceding kernel of the stream has finished)
   const int part = blockIdx.x % kParts, bg = blockIdx.x / kParts, b = bg / Hkv, g = bg - b * Hkv;
   const int j0 = part * G;  // this CTA's heads: j0 .. j0 + G - 1 of the group
   const int Hq = Hkv * GG;
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_mma_kernel(
   __shared__ uint32_t s_lohi[H][2];
   constexpr int kParts = GG / H;
   pdl_launch_dependents();  // the scan may launch now (it waits for this grid before reading the bracket)
+  pdl_wait();  // (PDL-launched: the preceding kernel of the stream, e.g. the one producing q, has finished)
   const int part = blockIdx.x % kParts, bg = blockIdx.x / kParts, b = bg / Hkv, g = bg - b * Hkv;
   const int j0 = part * H;
   const int Hq = Hkv * GG;
@@ -1842,13 +1844,13 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
                         : (multi ? sbs_sample_mma_kernel<kSampleThreads, 4, true> : sbs_sample_mma_kernel<kSampleThreads, 4, false>);
       e = set_smem(km, smem_m);
       if (e != cudaSuccess) return e;
-      e = launch_pdl(km, dim3(split ? 2 * BG : BG), dim3(snt), smem_m, st, false, q, geo.kv_dtype,
+      e = launch_pdl(km, dim3(split ? 2 * BG : BG), dim3(snt), smem_m, st, true, q, geo.kv_dtype,
                      reinterpret_cast<const uint16_t*>(sk), skc.channel_ids, kv.page_table, kv.seq_lens, geo.max_seq_len,
                      geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
     } else {
       e = set_smem(kern, smem_used);
       if (e != cudaSuccess) return e;
-      e = launch_pdl(kern, dim3(split ? 2 * BG : BG), dim3(snt), smem_used, st, false, q, geo.kv_dtype, sk, skc.channel_ids, C,
+      e = launch_pdl(kern, dim3(split ? 2 * BG : BG), dim3(snt), smem_used, st, true, q, geo.kv_dtype, sk, skc.channel_ids, C,
                      kv.page_table, kv.seq_lens, geo.max_seq_len, geo.max_pages, geo.Hkv, bud.dev(), w.thr, w.counters);
     }
     if (e != cudaSuccess) return e;
