@@ -553,14 +553,17 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_mma_kernel(
   for (int rr = 0; rr < (MULTI ? rounds : 1); ++rr) {
     if (rr) load_round(rr);
     score_round();
-    if (mine) {
+    // branch-free: a key that does not count goes to this lane's pad word of
+    // histogram 0 (pad words are never read, hidx skips them)
+    uint32_t* const dummy1 = hist1 + 65 * (lane + 1) - 1;
 #pragma unroll
-      for (int u = 0; u < kSampleSlots; ++u)
+    for (int u = 0; u < kSampleSlots; ++u)
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-          if (key[u][x] >= kmin && key[u][x] != 0u)
-            atomicAdd(&hist1[(hsel + (x & 1)) * kHistWords + hidx(key[u][x] >> kSampleSh1)], 1u);
-    }
+      for (int x = 0; x < 4; ++x) {
+        const uint32_t kk = key[u][x];
+        const bool ok = mine && kk >= kmin && kk != 0u;
+        atomicAdd(ok ? hist1 + (hsel + (x & 1)) * kHistWords + hidx(kk >> kSampleSh1) : dummy1, 1u);
+      }
   }
   __syncthreads();
   hist_group_sums<NT>(hist1, H, s_grp);
@@ -589,20 +592,24 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_mma_kernel(
       load_round(rr);
       score_round();
     }
-    if (mine) {
+    // only warps holding a key of a selected bin issue (warp-uniform test), to
+    // the lane's dummy word when its own key is not one
+    uint32_t* const dummy2 = s_grp + H * 32 + lane;
 #pragma unroll
-      for (int u = 0; u < kSampleSlots; ++u)
+    for (int u = 0; u < kSampleSlots; ++u)
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const uint32_t kk = key[u][x];
-          if (kk == 0u) continue;
-          const int j = hsel + (x & 1);
-          const int b1 = (int)(kk >> kSampleSh1);
-          const uint32_t b2 = (kk >> kSampleSh2) & 255u;
-          if (b1 == ((x & 1) ? bl1 : bl0)) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
-          if (b1 == ((x & 1) ? bh1 : bh0)) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+      for (int x = 0; x < 4; ++x) {
+        const uint32_t kk = key[u][x];
+        const int j = hsel + (x & 1);
+        const int b1 = (int)(kk >> kSampleSh1);
+        const uint32_t b2 = (kk >> kSampleSh2) & 255u;
+        const bool v = mine && kk != 0u;
+        const bool m0 = v && b1 == ((x & 1) ? bl1 : bl0), m1 = v && b1 == ((x & 1) ? bh1 : bh0);
+        if (__any_sync(0xffffffffu, m0 || m1)) {
+          atomicAdd(m0 ? hist2 + (j * 2 + 0) * 256 + b2 : dummy2, 1u);
+          atomicAdd(m1 ? hist2 + (j * 2 + 1) * 256 + b2 : dummy2, 1u);
         }
-    }
+      }
   }
   __syncthreads();
   if (warp < 2 * H) {
@@ -1838,7 +1845,7 @@ cudaError_t sbs_launch_t(const Geo& geo, const sd_paged_kv& kv, const sd_sketch&
     if (SkMma<G, Sk>::value && C == 8) {  // tensor-core sample (the scan's scores)
       const int H = split ? 2 : 4;
       const size_t smem_m = sizeof(uint32_t) * H * (kHistWords + 512) + (size_t)4 * kD * 4 + sizeof(int) * 8 +
-                            sizeof(uint32_t) * H * 32;
+                            sizeof(uint32_t) * (H * 32 + 32);  // group sums + 32 dummy words
       auto km = snt == 512 ? sbs_sample_mma_kernel<512, 4, false>
                 : split ? (multi ? sbs_sample_mma_kernel<kSampleThreads, 2, true> : sbs_sample_mma_kernel<kSampleThreads, 2, false>)
                         : (multi ? sbs_sample_mma_kernel<kSampleThreads, 4, true> : sbs_sample_mma_kernel<kSampleThreads, 4, false>);
