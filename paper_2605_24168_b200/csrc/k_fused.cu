@@ -399,13 +399,15 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) sbs_sample_kernel(
     }
 #pragma unroll
     for (int u = 0; u < kSampleSlots; ++u) {
-      if (tt[u] < 0) continue;
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int b1 = (int)(key[u][j] >> kSampleSh1);
         const uint32_t b2 = (key[u][j] >> kSampleSh2) & 255u;
-        if (b1 == bin_lo[j]) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
-        if (b1 == bin_hi[j]) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+        const bool m0 = tt[u] >= 0 && b1 == bin_lo[j], m1 = tt[u] >= 0 && b1 == bin_hi[j];
+        if (__any_sync(0xffffffffu, m0 || m1)) {  // only warps holding a key of a selected bin
+          if (m0) atomicAdd(&hist2[(j * 2 + 0) * 256 + b2], 1u);
+          if (m1) atomicAdd(&hist2[(j * 2 + 1) * 256 + b2], 1u);
+        }
       }
     }
   }
